@@ -1,0 +1,405 @@
+// tcgen05 / TMEM / TMA complex GEMM for sm_100a — the tensor-core hot loop of
+// the sliced contraction.
+//
+//   C[j][m][n] = 2^-(sA+sB) * Σ_k  A[ia(j)][m][k] · B[ib(j)][n][k]     (complex)
+//
+// Operands arrive as K-contiguous fp16 planes (re_hi, im_hi[, re_lo, im_lo]) of
+// the rescaled values x*2^s, written by the prep kernel.  The complex product
+// is formed from real MMAs on the planes, using the instruction descriptor's
+// negate-A bit for the -Ai·Bi term (no real embedding of B is materialised):
+//   Cr += Ar·Br - Ai·Bi,   Ci += Ar·Bi + Ai·Br.
+// Extended precision (3 passes) follows Eq. 8 with fp16
+// in place of tf32 (the 3xFP16 variant, L383-386): per real product
+//   x·y ≈ x_big·y_small + x_small·y_big + x_big·y_big   (small·small dropped,
+// small terms issued first), all accumulating in the fp32 TMEM accumulator.
+// Mixed mode (1 pass) keeps only big·big (L411, L442).
+//
+// Sparse einsum (Eq. 7) is the same kernel: batch j selects the A and
+// B slabs through the gather tables ia/ib — the "separate pointers for each
+// matrix of the batched GEMM" of L354 become TMA slab coordinates, so no
+// gathered copies are materialised.
+//
+// Structure (one CTA per SM, persistent, 6 warps):
+//   warp 0      TMA producer: 4D tensor-map loads (K, rows, slab, plane), box
+//               32x128, SWIZZLE_64B, into a STAGES-deep smem ring (mbarrier tx).
+//   warp 1      TMEM allocator (512 cols) + single-thread tcgen05.mma issuer,
+//               kind::f16, M=128 N=128 K=16, accumulators Cr|Ci = 256 TMEM
+//               columns, double-buffered across tiles; tcgen05.commit frees
+//               smem stages and hands full accumulators to the epilogue.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> scale by 2^-(sA+sB) ->
+//               float2 stores of C (or fused fp64 accumulate into the slice sum)
+//               + absmax of the result for the consumer's rescale.
+#include "tn_internal.h"
+#include <cstdio>
+
+namespace tn {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32;          // BK in complex k (64 B fp16 rows)
+constexpr int PLANE_TILE = 128 * BK * 2;            // 8 KiB per plane tile
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t TMEM_COLS = 512;
+
+template <int PASSES>
+struct Cfg {
+  static constexpr int PLANES = PASSES == 3 ? 4 : 2;
+  static constexpr int STAGE_BYTES = 2 * PLANES * PLANE_TILE;
+  static constexpr int STAGES = PASSES == 3 ? 3 : 6;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// instruction descriptor, kind::f16: D=f32 (bits 4-5 = 1), A=B=f16, K-major,
+// N>>3 at bits 17-22, M>>4 at bits 24-28; bit 13 = negate A.
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr uint32_t IDESC_NEG = IDESC | (1u << 13);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nTN_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra TN_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: 8-row atoms of 64 B rows,
+// SBO = 512 B between atoms, LBO unused (1), version 1 (sm_100), layout 4.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+#define TN_LD32(r, taddr)                                                                        \
+  asm volatile(                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),  \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),            \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),            \
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int PASSES>
+__global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
+  using C = Cfg<PASSES>;
+  constexpr int PLANES = C::PLANES, STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int kblocks = (args.K + BK - 1) / BK;
+  const int64_t per_j = (int64_t)args.tiles_m * args.tiles_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
+        const int j = (int)(tile / per_j);
+        const int rem = (int)(tile % per_j);
+        const int mt = rem / args.tiles_n, nt = rem % args.tiles_n;
+        const int sa = args.ia ? args.ia[j] : 0;
+        const int sb = args.ib ? args.ib[j] : 0;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* st = smem + stage * C::STAGE_BYTES;
+#pragma unroll
+          for (int p = 0; p < PLANES; ++p)
+            tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BK, mt * BM, sa, p);
+#pragma unroll
+          for (int p = 0; p < PLANES; ++p)
+            tma_load_4d(&args.mapB, st + (PLANES + p) * PLANE_TILE, &full[stage], kb * BK, nt * BN,
+                        sb, p);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[as], aphase ^ 1);
+        fence_after();
+        const uint32_t d_re = tmem_base + as * 256;
+        const uint32_t d_im = d_re + 128;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint32_t st = smem_u32(smem + stage * C::STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint32_t koff = kk * 32;   // 16 fp16 = 32 B along K inside the swizzle row
+            const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
+            const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
+            const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
+            const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
+            const uint32_t acc0 = (kb | kk) != 0;
+            if (PASSES == 3) {
+              const uint64_t arl = sdesc(st + 2 * PLANE_TILE + koff);
+              const uint64_t ail = sdesc(st + 3 * PLANE_TILE + koff);
+              const uint64_t brl = sdesc(st + (PLANES + 2) * PLANE_TILE + koff);
+              const uint64_t bil = sdesc(st + (PLANES + 3) * PLANE_TILE + koff);
+              // real part: Ar·Br - Ai·Bi  (small terms first, Eq. 8)
+              mma(d_re, ar, brl, IDESC, acc0);
+              mma(d_re, arl, br, IDESC, 1);
+              mma(d_re, ail, bi, IDESC_NEG, 1);
+              mma(d_re, ai, bil, IDESC_NEG, 1);
+              mma(d_re, ar, br, IDESC, 1);
+              mma(d_re, ai, bi, IDESC_NEG, 1);
+              // imaginary part: Ar·Bi + Ai·Br
+              mma(d_im, ar, bil, IDESC, acc0);
+              mma(d_im, arl, bi, IDESC, 1);
+              mma(d_im, ai, brl, IDESC, 1);
+              mma(d_im, ail, br, IDESC, 1);
+              mma(d_im, ar, bi, IDESC, 1);
+              mma(d_im, ai, br, IDESC, 1);
+            } else {
+              mma(d_re, ar, br, IDESC, acc0);
+              mma(d_re, ai, bi, IDESC_NEG, 1);
+              mma(d_im, ar, bi, IDESC, acc0);
+              mma(d_im, ai, br, IDESC, 1);
+            }
+          }
+          mma_commit(&empty[stage]);   // frees the smem stage when these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[as]);        // accumulator ready for the epilogue
+        if (++as == 2) {
+          as = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    const float scale = ldexpf(1.0f, -(*args.scaleA + *args.scaleB));
+    const bool vec_ok = (args.N % 2) == 0;
+    float amax = 0.f;
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
+      const int j = (int)(tile / per_j);
+      const int rem = (int)(tile % per_j);
+      const int mt = rem / args.tiles_n, nt = rem % args.tiles_n;
+      mbar_wait(&tfull[as], aphase);
+      fence_after();
+      const int m = mt * BM + row;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + as * 256;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t vr[32], vi[32];
+        TN_LD32(vr, tbase + c * 32);
+        TN_LD32(vi, tbase + 128 + c * 32);
+        tmem_wait_ld();
+        const int n0 = nt * BN + c * 32;
+        if (m < args.M && n0 < args.N) {
+          const int64_t base = ((int64_t)j * args.M + m) * (int64_t)args.N + n0;
+          const int cnt = min(32, args.N - n0);
+          if (args.acc) {
+            for (int i = 0; i < cnt; ++i) {
+              const float re = __uint_as_float(vr[i]) * scale, im = __uint_as_float(vi[i]) * scale;
+              double2 o = args.acc[base + i];
+              o.x += (double)re;
+              o.y += (double)im;
+              args.acc[base + i] = o;
+              amax = fmaxf(amax, fmaxf(fabsf(re), fabsf(im)));
+            }
+          } else if (vec_ok && cnt == 32) {
+            float4* dst = reinterpret_cast<float4*>(args.C + base);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float r0 = __uint_as_float(vr[2 * i]) * scale, i0 = __uint_as_float(vi[2 * i]) * scale;
+              const float r1 = __uint_as_float(vr[2 * i + 1]) * scale,
+                          i1 = __uint_as_float(vi[2 * i + 1]) * scale;
+              dst[i] = make_float4(r0, i0, r1, i1);
+              amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
+            }
+          } else {
+            for (int i = 0; i < cnt; ++i) {
+              const float re = __uint_as_float(vr[i]) * scale, im = __uint_as_float(vi[i]) * scale;
+              args.C[base + i] = make_float2(re, im);
+              amax = fmaxf(amax, fmaxf(fabsf(re), fabsf(im)));
+            }
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (++as == 2) {
+        as = 0;
+        aphase ^= 1;
+      }
+    }
+    if (args.absmax_out) {
+      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0 && amax > 0.f) atomicMax(args.absmax_out, __float_as_uint(amax));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+template <int PASSES>
+cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
+  static bool attr_set = false;
+  const int smem = Cfg<PASSES>::SMEM_BYTES;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
+  if (grid < 1) grid = 1;
+  cgemm_tcgen05_kernel<PASSES><<<(unsigned)grid, NUM_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s) {
+  return passes == 3 ? launch_impl<3>(a, num_sms, s) : launch_impl<1>(a, num_sms, s);
+}
+
+bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
+                      int planes, int box_rows, char* err, size_t errcap) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    snprintf(err, errcap, "cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)Kpad, (cuuint64_t)R, (cuuint64_t)G, (cuuint64_t)planes};
+  cuuint64_t strides[3] = {(cuuint64_t)(Kpad * 2), (cuuint64_t)(Kpad * 2 * R),
+                           (cuuint64_t)(Kpad * 2 * R * G)};
+  cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(err, errcap, "cuTensorMapEncodeTiled failed (%d): Kpad=%lld R=%lld G=%lld", (int)r,
+             (long long)Kpad, (long long)R, (long long)G);
+    return false;
+  }
+  return true;
+}
+
+}  // namespace tn

@@ -1,0 +1,239 @@
+// HBM-side kernels of the hot path (sm_100a):
+//   slice_select  — a2: slice index -> mixed-radix digits -> per-leaf offsets
+//                   (DESIGN R7: last sliced bond fastest)
+//   prep          — a3 + a6: permutation of a strided complex64 view into the
+//                   K-contiguous fp16 planes the tensor-core GEMM reads, with the
+//                   per-tensor power-of-two rescale (L403, L594) and the RN hi/lo
+//                   split of Eq. 8 (L367-377; 3xFP16 variant L383-386)
+//   einsum_simt   — Eq. 3 (L219-229) on CUDA cores for small / skinny steps, with
+//                   sparse-merge gather tables (Eq. 7) and fused fp64 accumulate
+//   gather_out    — a9: merged-configuration order -> caller sample order
+#include "tn_internal.h"
+
+namespace tn {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void copy_desc_to_smem(T* dst, const T* src) {
+  static_assert(sizeof(T) % 8 == 0, "desc size");
+  const int n = sizeof(T) / 8;
+  const uint64_t* s = reinterpret_cast<const uint64_t*>(src);
+  uint64_t* d = reinterpret_cast<uint64_t*>(dst);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = s[i];
+  __syncthreads();
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void block_absmax(float v, unsigned* out) {
+  __shared__ float red[32];
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float x = (l < (int)(blockDim.x >> 5)) ? red[l] : 0.f;
+    x = warp_max(x);
+    if (l == 0 && x > 0.f) atomicMax(out, __float_as_uint(x));
+  }
+}
+
+// ---------------------------------------------------------------- slice select
+__global__ void slice_select_kernel(const SliceDesc* __restrict__ d) {
+  __shared__ int64_t digit[64];
+  __shared__ int64_t t0;
+  if (threadIdx.x == 0) {
+    int64_t t = *d->counter;
+    t0 = t;
+    for (int p = d->n_sliced - 1; p >= 0; --p) {   // last sliced bond = fastest digit
+      digit[p] = t % d->dims[p];
+      t /= d->dims[p];
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < d->n_leaves; l += blockDim.x) {
+    int64_t off = 0;
+    for (int q = 0; q < d->n_terms; ++q)
+      if (d->term_leaf[q] == l) off += digit[d->term_p[q]] * d->term_stride[q];
+    d->leaf_off[l] = off;
+  }
+  for (int a = threadIdx.x; a < d->absmax_count; a += blockDim.x) d->absmax[d->absmax_first + a] = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) *d->counter = t0 + 1;
+}
+
+// ---------------------------------------------------------------- operand prep
+template <int PLANES>
+__global__ void __launch_bounds__(256) prep_kernel(const PrepDesc* __restrict__ gd,
+                                                   const int64_t* __restrict__ leaf_off,
+                                                   int64_t total) {
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  const float amax = __uint_as_float(*d.absmax_in);
+  int s = 0;
+  if (amax > 0.f) {
+    int e;
+    frexpf(amax, &e);            // amax = f * 2^e, f in [0.5, 1)
+    s = 15 - e;                  // amax * 2^s in [2^14, 2^15): inside fp16 range
+    s = max(-120, min(120, s));
+  }
+  const float scale = ldexpf(1.0f, s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d.scale_out = s;
+  const int64_t plane = d.plane_elems;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx % d.Kpad;
+    const int64_t rest = idx / d.Kpad;
+    const int64_t r = rest % d.R;
+    const int64_t g = rest / d.R;
+    float2 v = make_float2(0.f, 0.f);
+    if (k < d.K) {
+      int64_t off = g * d.g_stride;
+      int64_t t = r;
+      for (int i = d.nr - 1; i >= 0; --i) { off += (t % d.r_ext[i]) * d.r_s[i]; t /= d.r_ext[i]; }
+      t = k;
+      for (int i = d.nk - 1; i >= 0; --i) { off += (t % d.k_ext[i]) * d.k_s[i]; t /= d.k_ext[i]; }
+      v = src[off];
+    }
+    const float xr = v.x * scale, xi = v.y * scale;
+    const __half hr = __float2half_rn(xr), hi = __float2half_rn(xi);
+    d.dst[idx] = hr;
+    d.dst[plane + idx] = hi;
+    if (PLANES == 4) {   // residuals, RN (Eq. 8: small = rn(x - big))
+      d.dst[2 * plane + idx] = __float2half_rn(xr - __half2float(hr));
+      d.dst[3 * plane + idx] = __float2half_rn(xi - __half2float(hi));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- SIMT einsum
+__global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restrict__ gd,
+                                                     const int64_t* __restrict__ leaf_off,
+                                                     int64_t total) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  const int nk = d.nk;
+  const int64_t klast = nk > 0 ? d.k_ext[nk - 1] : 1;
+  const int64_t ka_last = nk > 0 ? d.k_sa[nk - 1] : 0;
+  const int64_t kb_last = nk > 0 ? d.k_sb[nk - 1] : 0;
+  const int64_t kouter = nk > 0 ? d.K / klast : 1;
+  float amax = 0.f;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = idx % d.N;
+    const int64_t t1 = idx / d.N;
+    const int64_t m = t1 % d.M;
+    const int64_t j = t1 / d.M;
+    int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs;
+    int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs;
+    int64_t t = m;
+    for (int i = d.nm - 1; i >= 0; --i) { ao += (t % d.m_ext[i]) * d.m_sa[i]; t /= d.m_ext[i]; }
+    t = n;
+    for (int i = d.nn - 1; i >= 0; --i) { bo += (t % d.n_ext[i]) * d.n_sb[i]; t /= d.n_ext[i]; }
+    float cr = 0.f, ci = 0.f;
+    for (int64_t ko = 0; ko < kouter; ++ko) {
+      int64_t ak = ao, bk = bo, u = ko;
+      for (int i = nk - 2; i >= 0; --i) {
+        const int64_t dg = u % d.k_ext[i];
+        u /= d.k_ext[i];
+        ak += dg * d.k_sa[i];
+        bk += dg * d.k_sb[i];
+      }
+      for (int64_t ki = 0; ki < klast; ++ki) {
+        const float2 a = A[ak + ki * ka_last];
+        const float2 b = B[bk + ki * kb_last];
+        cr = fmaf(a.x, b.x, cr);
+        cr = fmaf(-a.y, b.y, cr);
+        ci = fmaf(a.x, b.y, ci);
+        ci = fmaf(a.y, b.x, ci);
+      }
+    }
+    if (d.acc) {
+      double2 o = d.acc[idx];
+      o.x += (double)cr;
+      o.y += (double)ci;
+      d.acc[idx] = o;
+    } else {
+      d.C[idx] = make_float2(cr, ci);
+    }
+    amax = fmaxf(amax, fmaxf(fabsf(cr), fabsf(ci)));
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+__global__ void gather_out_kernel(const double2* __restrict__ acc, const int32_t* __restrict__ pos,
+                                  double2* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = acc[pos[i]];
+}
+
+int grid_for(int64_t total, int threads) {
+  int64_t b = (total + threads - 1) / threads;
+  const int64_t cap = 148 * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
+  slice_select_kernel<<<1, 256, 0, s>>>(d_desc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, const int64_t* leaf_off,
+                        cudaStream_t s) {
+  const int th = 256;
+  if (planes == 4)
+    prep_kernel<4><<<grid_for(total, th), th, 0, s>>>(d_desc, leaf_off, total);
+  else
+    prep_kernel<2><<<grid_for(total, th), th, 0, s>>>(d_desc, leaf_off, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_einsum(const EinsumDesc* d_desc, int64_t total, const int64_t* leaf_off,
+                          cudaStream_t s) {
+  const int th = 256;
+  einsum_kernel<<<grid_for(total, th), th, 0, s>>>(d_desc, leaf_off, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
+                              cudaStream_t s) {
+  gather_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(acc, pos, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tn
+
+namespace tn {
+namespace {
+__global__ void absmax_kernel(const float2* __restrict__ x, int64_t n, unsigned* out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = x[i];
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+}  // namespace
+
+cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  absmax_kernel<<<(unsigned)b, 256, 0, s>>>(x, n, out);
+  return cudaGetLastError();
+}
+}  // namespace tn

@@ -1,0 +1,1220 @@
+// Host side of the library: network validation, sparse-state tables, path replay
+// and step planning, slice bookkeeping (a2), buffer liveness,
+// the per-slice launch sequence (a3-a8), output mapping (a9) and the C ABI
+// declared in include/tn.h.  Every arithmetic step of a contraction runs in the
+// CUDA kernels of kernels.cu / gemm_tcgen05.cu; this file only plans and launches.
+#include "tn_internal.h"
+#include "tn.h"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+tn_status fail(tn_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+#define TN_CUDA(x)                                                                       \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(TN_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+constexpr int64_t GROUP = INT64_MIN;   // label of the merged open-group (sample) dim
+
+struct VDim {
+  int64_t label, ext, stride;
+};
+
+// A strided view of a live tensor.  The group dim (label GROUP) indexes the
+// tensor's merged open group: entry g <-> table[g] (sorted projections of the
+// samples onto `q`, qubit q[0] most significant).
+struct View {
+  int buf = 0;          // 0 = leaf buffer, 1 = arena
+  int64_t off = 0;      // element offset
+  int leaf = -1;        // leaf index (dynamic slice offset) or -1
+  std::vector<VDim> dims;
+  std::vector<int> q;
+  std::vector<uint64_t> table;
+  int absmax_slot = 0;
+  bool has_group() const { return !q.empty(); }
+  int64_t size() const {
+    int64_t s = 1;
+    for (auto& d : dims) s *= d.ext;
+    return s;
+  }
+};
+
+struct StepPlan {
+  int i = 0, j = 0;
+  bool merge = false, tc = false, final_step = false, swap = false;
+  int64_t J = 1, m = 1, n = 1, k = 1;
+  double tcc = 0, tmc = 0;
+  std::vector<int32_t> ia, ib;
+  int64_t ia_off = -1, ib_off = -1;     // offsets into the device table buffer
+  int64_t out_off = -1, out_elems = 0;  // arena element offset
+  View out;
+  // device descriptor indices
+  int einsum_idx = -1, prep_idx = -1;   // prep_idx: P at prep_idx, Q at prep_idx+1
+  tn::GemmArgs gemm;
+  int64_t prep_total[2] = {0, 0};
+  int64_t R[2] = {0, 0}, Kpad = 0, G[2] = {1, 1};
+  int in_slot[2] = {0, 0};
+};
+
+struct KStats {
+  int64_t launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+
+struct Pending {
+  cudaEvent_t a, b;
+  int family;
+  double flops, bytes;
+};
+
+}  // namespace
+
+struct tn_ctx {
+  int device = 0;
+  bool host_only = false;   // device = -1: plan/bookkeeping only, no CUDA calls
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  // network
+  bool loaded = false, pathed = false, planned = false;
+  int n_tensors = 0;
+  std::vector<std::vector<int64_t>> labels, dims;
+  std::vector<int64_t> data_off;             // complex offsets into host data
+  int64_t n_data = 0;
+  int n_open = 0;
+  std::vector<int64_t> open_labels;
+  std::unordered_map<int64_t, int> qubit_of;
+  std::unordered_map<int64_t, int64_t> dim_of;
+  std::unordered_map<int64_t, int> count_of;
+  int64_t n_samples = 0;
+  bool full_state = false;
+  std::vector<uint64_t> packed;              // packed samples (qubit 0 = MSB)
+  // leaves (after open-group gather)
+  std::vector<View> leaf_views;              // unsliced leaf views
+  std::vector<int64_t> leaf_src;             // device leaf element -> host complex index
+  std::vector<int64_t> leaf_begin;           // element offset of each leaf in leaf buffer
+  int64_t leaf_elems = 0;
+  std::vector<float> leaf_absmax;
+  float2* d_leaf = nullptr;
+  float2* h_leaf_pinned = nullptr;
+  // path / slices
+  std::vector<std::pair<int, int>> path;
+  std::vector<int64_t> sliced;
+  int64_t n_slices = 1;
+  // plan
+  std::vector<StepPlan> steps;
+  View root;
+  std::vector<int32_t> out_pos;
+  int64_t n_out = 0, acc_elems = 1;
+  double flops_per_slice = 0, tc_flops = 0, bytes_per_slice = 0, peak = 0;
+  int64_t arena_elems = 0, scratch_bytes = 0;
+  // device buffers
+  float2* d_arena = nullptr;
+  uint8_t* d_scratch = nullptr;
+  int32_t* d_tables = nullptr;
+  double2* d_acc = nullptr;
+  unsigned* d_absmax = nullptr;
+  int* d_scales = nullptr;
+  int64_t* d_leaf_off = nullptr;
+  int64_t* d_counter = nullptr;
+  int64_t* h_counter = nullptr;
+  int32_t* d_out_pos = nullptr;
+  tn::SliceDesc* d_slice_desc = nullptr;
+  int32_t* d_terms_i = nullptr;
+  int64_t* d_terms_s = nullptr;
+  tn::EinsumDesc* d_einsum = nullptr;
+  tn::PrepDesc* d_prep = nullptr;
+  float2* d_one = nullptr;
+  int64_t device_bytes = 0;
+  // profiling
+  bool profiling = false;
+  std::vector<Pending> pending;
+  KStats stats[4];
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+
+uint64_t project(uint64_t v, const std::vector<int>& q, int n_open) {
+  uint64_t r = 0;
+  for (int x : q) r = (r << 1) | ((v >> (n_open - 1 - x)) & 1ull);
+  return r;
+}
+
+std::vector<uint64_t> table_for(const tn_ctx* c, const std::vector<int>& q) {
+  std::vector<uint64_t> t;
+  t.reserve(c->packed.size());
+  for (uint64_t s : c->packed) t.push_back(project(s, q, c->n_open));
+  std::sort(t.begin(), t.end());
+  t.erase(std::unique(t.begin(), t.end()), t.end());
+  return t;
+}
+
+int64_t index_in(const std::vector<uint64_t>& t, uint64_t v) {
+  auto it = std::lower_bound(t.begin(), t.end(), v);
+  if (it == t.end() || *it != v) return -1;
+  return it - t.begin();
+}
+
+void free_dev(tn_ctx* c) {
+  if (c->host_only) { c->planned = false; return; }
+  void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
+                  c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
+                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_counter) cudaFreeHost(c->h_counter);
+  c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
+  c->d_absmax = nullptr; c->d_scales = nullptr; c->d_leaf_off = nullptr; c->d_counter = nullptr;
+  c->d_out_pos = nullptr; c->d_slice_desc = nullptr; c->d_terms_i = nullptr; c->d_terms_s = nullptr;
+  c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr; c->h_counter = nullptr;
+  c->planned = false;
+}
+
+template <typename T>
+tn_status dev_alloc(tn_ctx* c, T** p, size_t count) {
+  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(TN_ERR_RESOURCE, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  }
+  if (e != cudaSuccess) return fail(TN_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  c->device_bytes += bytes;
+  return TN_OK;
+}
+
+// merge adjacent dims whose strides chain (row-major runs) — single stride list
+void coalesce1(std::vector<VDim>& d) {
+  std::vector<VDim> o;
+  for (auto& x : d) {
+    if (x.ext == 1) continue;
+    if (!o.empty() && o.back().stride == x.ext * x.stride) {
+      o.back().ext *= x.ext;
+      o.back().stride = x.stride;
+    } else {
+      o.push_back(x);
+    }
+  }
+  d.swap(o);
+}
+
+struct KDim {
+  int64_t ext, sa, sb;
+};
+void coalesce2(std::vector<KDim>& d) {
+  std::vector<KDim> o;
+  for (auto& x : d) {
+    if (x.ext == 1) continue;
+    if (!o.empty() && o.back().sa == x.ext * x.sa && o.back().sb == x.ext * x.sb) {
+      o.back().ext *= x.ext;
+      o.back().sa = x.sa;
+      o.back().sb = x.sb;
+    } else {
+      o.push_back(x);
+    }
+  }
+  d.swap(o);
+}
+
+void contiguous_strides(std::vector<VDim>& d) {
+  int64_t s = 1;
+  for (int p = (int)d.size() - 1; p >= 0; --p) {
+    d[p].stride = s;
+    s *= d[p].ext;
+  }
+}
+
+// first-fit arena with liveness
+struct Arena {
+  std::vector<std::pair<int64_t, int64_t>> used;   // (offset, size), sorted
+  int64_t high = 0;
+  static int64_t align(int64_t x) { return (x + 31) & ~int64_t(31); }   // 256 B for complex64
+  int64_t alloc(int64_t n) {
+    n = align(std::max<int64_t>(n, 1));
+    int64_t at = 0;
+    size_t pos = 0;
+    for (; pos < used.size(); ++pos) {
+      if (used[pos].first - at >= n) break;
+      at = align(used[pos].first + used[pos].second);
+    }
+    used.insert(used.begin() + pos, {at, n});
+    high = std::max(high, at + n);
+    return at;
+  }
+  void release(int64_t off) {
+    for (size_t p = 0; p < used.size(); ++p)
+      if (used[p].first == off) {
+        used.erase(used.begin() + p);
+        return;
+      }
+  }
+};
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// ---------------------------------------------------------------- planning
+
+tn_status build_plan(tn_ctx* c) {
+  free_dev(c);
+  c->device_bytes = c->leaf_elems * sizeof(float2);
+  const int tc_big = env_int("TN_TC_MIN_BIG", 128);
+  const int tc_small = env_int("TN_TC_MIN_SMALL", 16);
+  const int tc_k = env_int("TN_TC_MIN_K", 16);
+  const int disable_tc = env_int("TN_DISABLE_TC", 0);
+  const int n_leaves = c->n_tensors;
+  const int n_steps = (int)c->path.size();
+
+  // leaf views with sliced bonds removed; dynamic offset terms
+  std::unordered_map<int64_t, int> slice_pos;
+  for (size_t p = 0; p < c->sliced.size(); ++p) slice_pos[c->sliced[p]] = (int)p;
+  std::vector<int32_t> term_leaf, term_p;
+  std::vector<int64_t> term_stride;
+  std::unordered_map<int, View> live;
+  for (int t = 0; t < n_leaves; ++t) {
+    View v = c->leaf_views[t];
+    std::vector<VDim> kept;
+    for (auto& d : v.dims) {
+      auto it = slice_pos.find(d.label);
+      if (it != slice_pos.end()) {
+        term_leaf.push_back(t);
+        term_p.push_back(it->second);
+        term_stride.push_back(d.stride);
+      } else {
+        kept.push_back(d);
+      }
+    }
+    v.dims = kept;
+    v.absmax_slot = t;
+    live[t] = v;
+  }
+
+  Arena arena;
+  std::vector<int32_t> tables;
+  int64_t scratch = 0;
+  c->steps.clear();
+  c->flops_per_slice = c->tc_flops = c->bytes_per_slice = c->peak = 0;
+  for (auto& kv : live) c->peak = std::max(c->peak, (double)kv.second.size());
+  int n_einsum = 0, n_prep = 0;
+
+  for (int s = 0; s < n_steps; ++s) {
+    StepPlan sp;
+    sp.i = c->path[s].first;
+    sp.j = c->path[s].second;
+    sp.final_step = (s == n_steps - 1);
+    View A = live[sp.i], B = live[sp.j];
+    sp.in_slot[0] = A.absmax_slot;
+    sp.in_slot[1] = B.absmax_slot;
+    // Eq. 3 set rule: δ = shared bond labels, γ = the rest
+    std::unordered_set<int64_t> lb;
+    for (auto& d : B.dims) if (d.label != GROUP) lb.insert(d.label);
+    std::vector<VDim> Kd_A, Kd_B, FA, FB;
+    std::unordered_set<int64_t> kset;
+    for (auto& d : A.dims)
+      if (d.label != GROUP && lb.count(d.label)) { Kd_A.push_back(d); kset.insert(d.label); }
+    for (auto& d : A.dims) if (!(d.label != GROUP && kset.count(d.label))) FA.push_back(d);
+    for (auto& d : Kd_A)
+      for (auto& e : B.dims) if (e.label == d.label) Kd_B.push_back(e);
+    for (auto& d : B.dims) if (!(d.label != GROUP && kset.count(d.label))) FB.push_back(d);
+    sp.merge = A.has_group() && B.has_group();
+    VDim gA{GROUP, 1, 0}, gB{GROUP, 1, 0};
+    View out;
+    if (sp.merge) {
+      // Eq. 7: merged configurations = unique sample projections onto qA ∪ qB
+      for (auto it = FA.begin(); it != FA.end(); ++it) if (it->label == GROUP) { gA = *it; FA.erase(it); break; }
+      for (auto it = FB.begin(); it != FB.end(); ++it) if (it->label == GROUP) { gB = *it; FB.erase(it); break; }
+      std::vector<int> q = A.q;
+      q.insert(q.end(), B.q.begin(), B.q.end());
+      std::sort(q.begin(), q.end());
+      std::vector<uint64_t> tq = table_for(c, q);
+      // map each merged config to its projections (from the samples: the map is a function)
+      std::unordered_map<uint64_t, std::pair<uint64_t, uint64_t>> proj;
+      proj.reserve(tq.size() * 2);
+      for (uint64_t smp : c->packed)
+        proj.emplace(project(smp, q, c->n_open),
+                     std::make_pair(project(smp, A.q, c->n_open), project(smp, B.q, c->n_open)));
+      sp.ia.resize(tq.size());
+      sp.ib.resize(tq.size());
+      for (size_t f = 0; f < tq.size(); ++f) {
+        auto pr = proj[tq[f]];
+        int64_t a = index_in(A.table, pr.first), b = index_in(B.table, pr.second);
+        if (a < 0 || b < 0) return fail(TN_ERR_INTERNAL, "merge table lookup failed");
+        sp.ia[f] = (int32_t)a;
+        sp.ib[f] = (int32_t)b;
+      }
+      sp.J = (int64_t)tq.size();
+      out.q = q;
+      out.table = tq;
+    } else if (A.has_group()) {
+      out.q = A.q;
+      out.table = A.table;
+    } else if (B.has_group()) {
+      out.q = B.q;
+      out.table = B.table;
+    }
+    for (auto& d : FA) sp.m *= d.ext;
+    for (auto& d : FB) sp.n *= d.ext;
+    for (auto& d : Kd_A) sp.k *= d.ext;
+    sp.tcc = 8.0 * (double)sp.J * (double)sp.m * (double)sp.n * (double)sp.k;   // Eq. 4
+    const int64_t out_elems = sp.J * sp.m * sp.n;
+    sp.tmc = 8.0 * ((double)A.size() + (double)B.size() + (double)out_elems);    // Eq. 5
+    c->flops_per_slice += sp.tcc;
+    c->bytes_per_slice += sp.tmc;
+    c->peak = std::max(c->peak, (double)out_elems);
+
+    const int64_t big = std::max(sp.m, sp.n), small = std::min(sp.m, sp.n);
+    sp.tc = !disable_tc && big >= tc_big && small >= tc_small && sp.k >= tc_k && !sp.final_step &&
+            sp.m < INT32_MAX && sp.n < INT32_MAX && sp.k < INT32_MAX && sp.J < INT32_MAX;
+    sp.swap = sp.tc && sp.n > sp.m;   // tensor-core M side = larger free extent
+
+    // output layout: [J][P dims][Q dims], P = A side unless swapped
+    std::vector<VDim> od;
+    if (sp.merge) od.push_back({GROUP, sp.J, 0});
+    const auto& P = sp.swap ? FB : FA;
+    const auto& Q = sp.swap ? FA : FB;
+    for (auto& d : P) od.push_back({d.label, d.ext, 0});
+    for (auto& d : Q) od.push_back({d.label, d.ext, 0});
+    contiguous_strides(od);
+    out.dims = od;
+    out.buf = 1;
+    out.absmax_slot = n_leaves + s;
+
+    if (sp.merge) {
+      sp.ia_off = (int64_t)tables.size();
+      tables.insert(tables.end(), sp.ia.begin(), sp.ia.end());
+      sp.ib_off = (int64_t)tables.size();
+      tables.insert(tables.end(), sp.ib.begin(), sp.ib.end());
+    }
+    if (!sp.final_step) {
+      sp.out_elems = out_elems;
+      sp.out_off = arena.alloc(out_elems);
+      out.off = sp.out_off;
+    }
+    if (sp.tc) {
+      sp.einsum_idx = -1;
+      sp.prep_idx = n_prep;
+      n_prep += 2;
+      sp.Kpad = (sp.k + 7) / 8 * 8;
+      sp.R[0] = sp.swap ? sp.n : sp.m;
+      sp.R[1] = sp.swap ? sp.m : sp.n;
+      sp.G[0] = sp.merge ? (sp.swap ? gB.ext : gA.ext) : 1;
+      sp.G[1] = sp.merge ? (sp.swap ? gA.ext : gB.ext) : 1;
+      int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
+      int64_t bytes1 = (4 * sp.G[1] * sp.R[1] * sp.Kpad * 2 + 1023) / 1024 * 1024;
+      scratch = std::max(scratch, bytes0 + bytes1);
+      c->tc_flops += sp.tcc;
+    } else {
+      sp.einsum_idx = n_einsum++;
+    }
+    // release consumed arena inputs (their only consumer is this step)
+    if (A.buf == 1) arena.release(A.off);
+    if (B.buf == 1) arena.release(B.off);
+    live.erase(sp.j);
+    live[sp.i] = out;
+    sp.out = out;
+    c->steps.push_back(sp);
+  }
+
+  // root
+  if (n_steps == 0) return fail(TN_ERR_USAGE, "networks with a single tensor are not supported");
+  c->root = c->steps.back().out;
+  for (auto& d : c->root.dims)
+    if (d.label != GROUP) return fail(TN_ERR_DATA, "bond label left uncontracted at the root");
+  if (c->n_open > 0) {
+    std::vector<int> all(c->n_open);
+    std::iota(all.begin(), all.end(), 0);
+    if (c->root.q != all) return fail(TN_ERR_DATA, "root group does not cover all open bonds");
+    c->acc_elems = (int64_t)c->root.table.size();
+    c->out_pos.resize(c->n_samples);
+    for (int64_t s = 0; s < c->n_samples; ++s)
+      c->out_pos[s] = (int32_t)index_in(c->root.table, c->packed[s]);
+    c->n_out = c->n_samples;
+  } else {
+    c->acc_elems = 1;
+    c->out_pos.assign(1, 0);
+    c->n_out = 1;
+  }
+  c->arena_elems = arena.high;
+  c->scratch_bytes = scratch;
+  if (c->host_only) {
+    c->planned = true;
+    return TN_OK;
+  }
+
+  // ------------------------------------------------------------ device buffers
+  tn_status st;
+  if ((st = dev_alloc(c, &c->d_arena, (size_t)std::max<int64_t>(c->arena_elems, 1)))) return st;
+  if ((st = dev_alloc(c, &c->d_scratch, (size_t)std::max<int64_t>(scratch, 1024)))) return st;
+  if ((st = dev_alloc(c, &c->d_tables, std::max<size_t>(tables.size(), 1)))) return st;
+  if ((st = dev_alloc(c, &c->d_acc, (size_t)c->acc_elems))) return st;
+  if ((st = dev_alloc(c, &c->d_absmax, (size_t)(n_leaves + n_steps)))) return st;
+  if ((st = dev_alloc(c, &c->d_scales, (size_t)(2 * n_steps)))) return st;
+  if ((st = dev_alloc(c, &c->d_leaf_off, (size_t)n_leaves))) return st;
+  if ((st = dev_alloc(c, &c->d_counter, 1))) return st;
+  if ((st = dev_alloc(c, &c->d_out_pos, c->out_pos.size()))) return st;
+  if ((st = dev_alloc(c, &c->d_slice_desc, 1))) return st;
+  if ((st = dev_alloc(c, &c->d_terms_i, std::max<size_t>(2 * term_leaf.size(), 1)))) return st;
+  if ((st = dev_alloc(c, &c->d_terms_s, std::max<size_t>(term_stride.size(), 1)))) return st;
+  if ((st = dev_alloc(c, &c->d_einsum, (size_t)std::max(n_einsum, 1)))) return st;
+  if ((st = dev_alloc(c, &c->d_prep, (size_t)std::max(n_prep, 1)))) return st;
+  if ((st = dev_alloc(c, &c->d_one, 1))) return st;
+  TN_CUDA(cudaMallocHost(&c->h_counter, sizeof(int64_t)));
+  cudaStream_t sm = c->stream;
+  if (!tables.empty())
+    TN_CUDA(cudaMemcpyAsync(c->d_tables, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice, sm));
+  TN_CUDA(cudaMemcpyAsync(c->d_out_pos, c->out_pos.data(), c->out_pos.size() * 4,
+                          cudaMemcpyHostToDevice, sm));
+  TN_CUDA(cudaMemsetAsync(c->d_acc, 0, c->acc_elems * sizeof(double2), sm));
+  TN_CUDA(cudaMemsetAsync(c->d_leaf_off, 0, n_leaves * sizeof(int64_t), sm));
+  {
+    std::vector<unsigned> am(n_leaves + n_steps, 0u);
+    for (int t = 0; t < n_leaves; ++t) memcpy(&am[t], &c->leaf_absmax[t], 4);
+    TN_CUDA(cudaMemcpyAsync(c->d_absmax, am.data(), am.size() * 4, cudaMemcpyHostToDevice, sm));
+    float2 one = make_float2(1.f, 0.f);
+    TN_CUDA(cudaMemcpyAsync(c->d_one, &one, sizeof(one), cudaMemcpyHostToDevice, sm));
+  }
+  // slice descriptor
+  {
+    if (c->sliced.size() > 64) return fail(TN_ERR_DATA, "at most 64 sliced bonds");
+    tn::SliceDesc sd{};
+    sd.n_sliced = (int32_t)c->sliced.size();
+    for (size_t p = 0; p < c->sliced.size(); ++p) sd.dims[p] = c->dim_of[c->sliced[p]];
+    sd.n_terms = (int32_t)term_leaf.size();
+    std::vector<int32_t> ti(term_leaf);
+    ti.insert(ti.end(), term_p.begin(), term_p.end());
+    if (!ti.empty())
+      TN_CUDA(cudaMemcpyAsync(c->d_terms_i, ti.data(), ti.size() * 4, cudaMemcpyHostToDevice, sm));
+    if (!term_stride.empty())
+      TN_CUDA(cudaMemcpyAsync(c->d_terms_s, term_stride.data(), term_stride.size() * 8,
+                              cudaMemcpyHostToDevice, sm));
+    sd.term_leaf = c->d_terms_i;
+    sd.term_p = c->d_terms_i + term_leaf.size();
+    sd.term_stride = c->d_terms_s;
+    sd.n_leaves = n_leaves;
+    sd.leaf_off = c->d_leaf_off;
+    sd.counter = c->d_counter;
+    sd.absmax = c->d_absmax;
+    sd.absmax_first = n_leaves;
+    sd.absmax_count = n_steps;
+    TN_CUDA(cudaMemcpyAsync(c->d_slice_desc, &sd, sizeof(sd), cudaMemcpyHostToDevice, sm));
+  }
+  // per-step device descriptors
+  std::vector<tn::EinsumDesc> eds(std::max(n_einsum, 1));
+  std::vector<tn::PrepDesc> pds(std::max(n_prep, 1));
+  auto base_of = [&](const View& v) -> const float2* { return v.buf == 0 ? c->d_leaf : c->d_arena; };
+  // rebuild the live views to fill descriptors (same replay as above)
+  live.clear();
+  for (int t = 0; t < n_leaves; ++t) {
+    View v = c->leaf_views[t];
+    std::vector<VDim> kept;
+    for (auto& d : v.dims) if (!slice_pos.count(d.label)) kept.push_back(d);
+    v.dims = kept;
+    v.absmax_slot = t;
+    live[t] = v;
+  }
+  char errbuf[256];
+  for (int s = 0; s < n_steps; ++s) {
+    StepPlan& sp = c->steps[s];
+    View A = live[sp.i], B = live[sp.j];
+    std::unordered_set<int64_t> lb;
+    for (auto& d : B.dims) if (d.label != GROUP) lb.insert(d.label);
+    std::vector<VDim> FA, FB;
+    std::vector<KDim> K;
+    std::unordered_set<int64_t> kset;
+    VDim gA{GROUP, 1, 0}, gB{GROUP, 1, 0};
+    for (auto& d : A.dims)
+      if (d.label != GROUP && lb.count(d.label)) {
+        kset.insert(d.label);
+        int64_t sb = 0;
+        for (auto& e : B.dims) if (e.label == d.label) sb = e.stride;
+        K.push_back({d.ext, d.stride, sb});
+      }
+    for (auto& d : A.dims) {
+      if (d.label != GROUP && kset.count(d.label)) continue;
+      if (sp.merge && d.label == GROUP) { gA = d; continue; }
+      FA.push_back(d);
+    }
+    for (auto& d : B.dims) {
+      if (d.label != GROUP && kset.count(d.label)) continue;
+      if (sp.merge && d.label == GROUP) { gB = d; continue; }
+      FB.push_back(d);
+    }
+    coalesce1(FA);
+    coalesce1(FB);
+    coalesce2(K);
+    if ((int)FA.size() > TN_MAXD || (int)FB.size() > TN_MAXD || (int)K.size() > TN_MAXD)
+      return fail(TN_ERR_INTERNAL, "step " + std::to_string(s) + ": too many non-coalescable dims");
+    unsigned* absmax_out = sp.final_step ? nullptr : c->d_absmax + (n_leaves + s);
+    float2* Cptr = sp.final_step ? nullptr : c->d_arena + sp.out_off;
+    if (!sp.tc) {
+      tn::EinsumDesc& e = eds[sp.einsum_idx];
+      memset(&e, 0, sizeof(e));
+      e.A = base_of(A); e.B = base_of(B); e.C = Cptr;
+      e.a_off = A.off; e.b_off = B.off;
+      e.a_leaf = A.buf == 0 ? A.leaf : -1;
+      e.b_leaf = B.buf == 0 ? B.leaf : -1;
+      e.J = sp.J;
+      e.ia = sp.merge ? c->d_tables + sp.ia_off : nullptr;
+      e.ib = sp.merge ? c->d_tables + sp.ib_off : nullptr;
+      e.a_gs = gA.stride; e.b_gs = gB.stride;
+      e.M = sp.m; e.N = sp.n; e.K = sp.k;
+      e.nm = (int)FA.size(); e.nn = (int)FB.size(); e.nk = (int)K.size();
+      for (int p = 0; p < e.nm; ++p) { e.m_ext[p] = FA[p].ext; e.m_sa[p] = FA[p].stride; }
+      for (int p = 0; p < e.nn; ++p) { e.n_ext[p] = FB[p].ext; e.n_sb[p] = FB[p].stride; }
+      for (int p = 0; p < e.nk; ++p) { e.k_ext[p] = K[p].ext; e.k_sa[p] = K[p].sa; e.k_sb[p] = K[p].sb; }
+      e.absmax_out = absmax_out;
+      e.acc = sp.final_step ? c->d_acc : nullptr;
+    } else {
+      // P operand = A side unless swapped; both share the canonical K order
+      for (int side = 0; side < 2; ++side) {
+        const bool fromA = (side == 0) != sp.swap;
+        const View& V = fromA ? A : B;
+        const auto& F = fromA ? FA : FB;
+        tn::PrepDesc& p = pds[sp.prep_idx + side];
+        memset(&p, 0, sizeof(p));
+        p.src = base_of(V);
+        p.off = V.off;
+        p.leaf = V.buf == 0 ? V.leaf : -1;
+        p.G = sp.G[side];
+        p.R = sp.R[side];
+        p.K = sp.k;
+        p.Kpad = sp.Kpad;
+        p.g_stride = sp.merge ? (fromA ? gA.stride : gB.stride) : 0;
+        p.nr = (int)F.size();
+        for (int d = 0; d < p.nr; ++d) { p.r_ext[d] = F[d].ext; p.r_s[d] = F[d].stride; }
+        std::vector<VDim> kd;
+        for (auto& x : K) kd.push_back({0, x.ext, fromA ? x.sa : x.sb});
+        // (K already coalesced jointly; keep as is)
+        p.nk = (int)kd.size();
+        for (int d = 0; d < p.nk; ++d) { p.k_ext[d] = kd[d].ext; p.k_s[d] = kd[d].stride; }
+        int64_t off0 = 0;
+        int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
+        if (side == 1) off0 = bytes0;
+        p.dst = reinterpret_cast<__half*>(c->d_scratch + off0);
+        p.plane_elems = sp.G[side] * sp.R[side] * sp.Kpad;
+        p.absmax_in = c->d_absmax + V.absmax_slot;
+        p.scale_out = c->d_scales + 2 * s + side;
+        sp.prep_total[side] = p.plane_elems;
+        CUtensorMap* map = side == 0 ? &sp.gemm.mapA : &sp.gemm.mapB;
+        if (!tn::encode_plane_map(map, p.dst, sp.Kpad, sp.R[side], sp.G[side], 4, 128, errbuf,
+                                  sizeof(errbuf)))
+          return fail(TN_ERR_INTERNAL, errbuf);
+      }
+      tn::GemmArgs& g = sp.gemm;
+      g.J = (int32_t)sp.J;
+      g.M = (int32_t)sp.R[0];
+      g.N = (int32_t)sp.R[1];
+      g.K = (int32_t)sp.k;
+      const int32_t* ta = sp.merge ? c->d_tables + sp.ia_off : nullptr;
+      const int32_t* tb = sp.merge ? c->d_tables + sp.ib_off : nullptr;
+      g.ia = sp.swap ? tb : ta;
+      g.ib = sp.swap ? ta : tb;
+      g.C = Cptr;
+      g.scaleA = c->d_scales + 2 * s;
+      g.scaleB = c->d_scales + 2 * s + 1;
+      g.absmax_out = absmax_out;
+      g.acc = sp.final_step ? c->d_acc : nullptr;
+      g.tiles_m = (int32_t)((sp.R[0] + 127) / 128);
+      g.tiles_n = (int32_t)((sp.R[1] + 127) / 128);
+      g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * sp.J;
+    }
+    live.erase(sp.j);
+    live[sp.i] = sp.out;
+  }
+  if (n_einsum) TN_CUDA(cudaMemcpyAsync(c->d_einsum, eds.data(), n_einsum * sizeof(tn::EinsumDesc),
+                                        cudaMemcpyHostToDevice, sm));
+  if (n_prep) TN_CUDA(cudaMemcpyAsync(c->d_prep, pds.data(), n_prep * sizeof(tn::PrepDesc),
+                                      cudaMemcpyHostToDevice, sm));
+  TN_CUDA(cudaStreamSynchronize(sm));
+  c->planned = true;
+  return TN_OK;
+}
+
+// ---------------------------------------------------------------- execution
+
+struct Timer {
+  tn_ctx* c;
+  int family;
+  double flops, bytes;
+  cudaEvent_t a{}, b{};
+  Timer(tn_ctx* c_, int f, double fl, double by) : c(c_), family(f), flops(fl), bytes(by) {
+    c->stats[f].launches++;
+    if (c->profiling) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Timer() {
+    if (c->profiling) {
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({a, b, family, flops, bytes});
+    }
+  }
+};
+
+tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int topk) {
+  cudaStream_t sm = c->stream;
+  // mixed precision: the top-k tensor-core steps by T_cc run 1-pass (§4.3, Table 3)
+  std::vector<int> passes(c->steps.size(), 3);
+  if (prec == TN_PREC_MIXED && topk > 0) {
+    std::vector<int> tcs;
+    for (size_t s = 0; s < c->steps.size(); ++s) if (c->steps[s].tc) tcs.push_back((int)s);
+    std::stable_sort(tcs.begin(), tcs.end(),
+                     [&](int a, int b) { return c->steps[a].tcc > c->steps[b].tcc; });
+    for (int r = 0; r < (int)tcs.size() && r < topk; ++r) passes[tcs[r]] = 1;
+  }
+  *c->h_counter = t0;
+  TN_CUDA(cudaMemcpyAsync(c->d_counter, c->h_counter, sizeof(int64_t), cudaMemcpyHostToDevice, sm));
+  for (int64_t t = t0; t < t1; ++t) {
+    {
+      Timer tm(c, 3, 0, 0);
+      TN_CUDA(tn::launch_slice_select(c->d_slice_desc, sm));
+    }
+    for (size_t s = 0; s < c->steps.size(); ++s) {
+      StepPlan& sp = c->steps[s];
+      if (!sp.tc) {
+        Timer tm(c, 2, sp.tcc, sp.tmc);
+        TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.J * sp.m * sp.n, c->d_leaf_off, sm));
+      } else {
+        const int ps = passes[s];
+        const int planes = ps == 3 ? 4 : 2;
+        for (int side = 0; side < 2; ++side) {
+          Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes));
+          TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
+                                  c->d_leaf_off, sm));
+        }
+        Timer tm(c, 0, sp.tcc, sp.tmc);
+        TN_CUDA(tn::launch_gemm(sp.gemm, ps, c->num_sms, sm));
+      }
+    }
+  }
+  return TN_OK;
+}
+
+tn_status check_planned(tn_ctx* c, bool need_device = true) {
+  if (!c) return fail(TN_ERR_USAGE, "null context");
+  if (!c->planned) return fail(TN_ERR_USAGE, "call tn_set_slices after tn_set_path first");
+  if (need_device && c->host_only) return fail(TN_ERR_USAGE, "host-only context (device -1) cannot execute");
+  return TN_OK;
+}
+
+// leaf layout: [group][remaining labels...] row-major; device element e <- host complex leaf_src[e]
+tn_status build_leaves(tn_ctx* c) {
+  c->leaf_views.assign(c->n_tensors, View());
+  c->leaf_src.clear();
+  c->leaf_begin.assign(c->n_tensors, 0);
+  int64_t cur = 0;
+  for (int t = 0; t < c->n_tensors; ++t) {
+    const auto& L = c->labels[t];
+    const auto& D = c->dims[t];
+    const int r = (int)L.size();
+    std::vector<int64_t> hstride(r);
+    int64_t s = 1;
+    for (int p = r - 1; p >= 0; --p) { hstride[p] = s; s *= D[p]; }
+    std::vector<int> open_pos, rest_pos;
+    for (int p = 0; p < r; ++p) (c->qubit_of.count(L[p]) ? open_pos : rest_pos).push_back(p);
+    std::sort(open_pos.begin(), open_pos.end(),
+              [&](int a, int b) { return c->qubit_of[L[a]] < c->qubit_of[L[b]]; });
+    View v;
+    v.buf = 0;
+    v.leaf = t;
+    v.off = cur;
+    std::vector<uint64_t> table{0};
+    if (!open_pos.empty()) {
+      for (int p : open_pos) v.q.push_back(c->qubit_of[L[p]]);
+      table = table_for(c, v.q);
+      v.table = table;
+    }
+    int64_t rest_elems = 1;
+    for (int p : rest_pos) rest_elems *= D[p];
+    if (!open_pos.empty()) v.dims.push_back({GROUP, (int64_t)table.size(), 0});
+    for (int p : rest_pos) v.dims.push_back({L[p], D[p], 0});
+    contiguous_strides(v.dims);
+    c->leaf_begin[t] = cur;
+    for (size_t g = 0; g < table.size(); ++g) {
+      int64_t base = c->data_off[t];
+      const int nq = (int)open_pos.size();
+      for (int a = 0; a < nq; ++a) base += (int64_t)((table[g] >> (nq - 1 - a)) & 1ull) * hstride[open_pos[a]];
+      // enumerate rest digits row-major
+      std::vector<int64_t> dig(rest_pos.size(), 0);
+      for (int64_t e = 0; e < rest_elems; ++e) {
+        int64_t off = base;
+        for (size_t a = 0; a < rest_pos.size(); ++a) off += dig[a] * hstride[rest_pos[a]];
+        c->leaf_src.push_back(off);
+        for (int a = (int)rest_pos.size() - 1; a >= 0; --a) {
+          if (++dig[a] < D[rest_pos[a]]) break;
+          dig[a] = 0;
+        }
+      }
+    }
+    cur += (int64_t)table.size() * rest_elems;
+    c->leaf_views[t] = v;
+  }
+  c->leaf_elems = cur;
+  return TN_OK;
+}
+
+tn_status upload_leaves(tn_ctx* c, const double* data) {
+  if (!c->h_leaf_pinned) TN_CUDA(cudaMallocHost(&c->h_leaf_pinned, std::max<int64_t>(c->leaf_elems, 1) * sizeof(float2)));
+  if (!c->d_leaf) TN_CUDA(cudaMalloc(&c->d_leaf, std::max<int64_t>(c->leaf_elems, 1) * sizeof(float2)));
+  // the previous upload may still be in flight from the pinned buffer
+  TN_CUDA(cudaStreamSynchronize(c->stream));
+  c->leaf_absmax.assign(c->n_tensors, 0.f);
+  for (int t = 0; t < c->n_tensors; ++t) {
+    const int64_t b = c->leaf_begin[t];
+    const int64_t e = (t + 1 < c->n_tensors) ? c->leaf_begin[t + 1] : c->leaf_elems;
+    float m = 0.f;
+    for (int64_t x = b; x < e; ++x) {
+      const int64_t src = c->leaf_src[x];
+      float2 v = make_float2((float)data[2 * src], (float)data[2 * src + 1]);
+      c->h_leaf_pinned[x] = v;
+      m = std::max(m, std::max(std::fabs(v.x), std::fabs(v.y)));
+    }
+    c->leaf_absmax[t] = m;
+  }
+  TN_CUDA(cudaMemcpyAsync(c->d_leaf, c->h_leaf_pinned, c->leaf_elems * sizeof(float2),
+                          cudaMemcpyHostToDevice, c->stream));
+  if (c->d_absmax) {
+    TN_CUDA(cudaMemcpyAsync(c->d_absmax, c->leaf_absmax.data(), c->n_tensors * 4,
+                            cudaMemcpyHostToDevice, c->stream));
+  }
+  return TN_OK;
+}
+
+void json_u64_list(std::string& o, const std::vector<int32_t>& v) {
+  if (v.size() <= 65536) {
+    o += "[";
+    for (size_t i = 0; i < v.size(); ++i) { if (i) o += ","; o += std::to_string(v[i]); }
+    o += "]";
+  } else {
+    uint64_t h = 1469598103934665603ull;
+    for (int32_t x : v) { h ^= (uint32_t)x; h *= 1099511628211ull; }
+    o += "{\"len\":" + std::to_string(v.size()) + ",\"fnv1a\":\"" + std::to_string(h) + "\"}";
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* tn_last_error(void) { return g_err.c_str(); }
+const char* tn_version(void) { return "tn-b200 0.1 (sm_100a tcgen05)"; }
+
+tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
+  if (!out) return fail(TN_ERR_USAGE, "out is NULL");
+  *out = nullptr;
+  if (device == -1) {
+    tn_ctx* c = new tn_ctx();
+    c->host_only = true;
+    c->device = -1;
+    *out = c;
+    return TN_OK;
+  }
+  int n = 0;
+  TN_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(TN_ERR_USAGE, "bad device index");
+  TN_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  TN_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(TN_ERR_CUDA, std::string("sm_100a device required, got ") + prop.name);
+  tn_ctx* c = new tn_ctx();
+  c->device = device;
+  c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  c->num_sms = prop.multiProcessorCount;
+  *out = c;
+  return TN_OK;
+}
+
+void tn_destroy(tn_ctx* c) {
+  if (!c) return;
+  if (c->host_only) { delete c; return; }
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  free_dev(c);
+  if (c->d_leaf) cudaFree(c->d_leaf);
+  if (c->h_leaf_pinned) cudaFreeHost(c->h_leaf_pinned);
+  delete c;
+}
+
+tn_status tn_load_network(tn_ctx* c, int32_t n_tensors, const int32_t* ranks, const int64_t* labels,
+                          const int64_t* dims, const double* data, int32_t n_open,
+                          const int64_t* open_labels, int64_t n_samples, const uint8_t* samples) {
+  if (!c) return fail(TN_ERR_USAGE, "null context");
+  if (n_tensors < 1 || !ranks || !data) return fail(TN_ERR_USAGE, "bad network arguments");
+  if (!c->host_only) TN_CUDA(cudaSetDevice(c->device));
+  free_dev(c);
+  c->loaded = c->pathed = false;
+  c->n_tensors = n_tensors;
+  c->labels.assign(n_tensors, {});
+  c->dims.assign(n_tensors, {});
+  c->data_off.assign(n_tensors, 0);
+  c->dim_of.clear();
+  c->count_of.clear();
+  c->qubit_of.clear();
+  int64_t li = 0, doff = 0;
+  for (int t = 0; t < n_tensors; ++t) {
+    if (ranks[t] < 0) return fail(TN_ERR_DATA, "negative rank");
+    int64_t sz = 1;
+    std::unordered_set<int64_t> seen;
+    for (int p = 0; p < ranks[t]; ++p, ++li) {
+      const int64_t l = labels[li], d = dims[li];
+      if (l == GROUP) return fail(TN_ERR_DATA, "reserved label value");
+      if (d < 1) return fail(TN_ERR_DATA, "dimension < 1");
+      if (!seen.insert(l).second)
+        return fail(TN_ERR_DATA, "label " + std::to_string(l) + " repeated in tensor " + std::to_string(t));
+      auto it = c->dim_of.find(l);
+      if (it != c->dim_of.end() && it->second != d)
+        return fail(TN_ERR_DATA, "dimension mismatch on label " + std::to_string(l));
+      c->dim_of[l] = d;
+      c->count_of[l]++;
+      c->labels[t].push_back(l);
+      c->dims[t].push_back(d);
+      sz *= d;
+    }
+    c->data_off[t] = doff;
+    doff += sz;
+  }
+  c->n_data = doff;
+  if (n_open < 0 || n_open > 64) return fail(TN_ERR_DATA, "n_open must be in [0, 64]");
+  c->n_open = n_open;
+  c->open_labels.assign(open_labels, open_labels + n_open);
+  for (int q = 0; q < n_open; ++q) {
+    const int64_t l = open_labels[q];
+    if (!c->count_of.count(l) || c->count_of[l] != 1)
+      return fail(TN_ERR_DATA, "open label " + std::to_string(l) + " must appear on exactly one tensor");
+    if (c->dim_of[l] != 2) return fail(TN_ERR_DATA, "open bonds must have dimension 2");
+    if (c->qubit_of.count(l)) return fail(TN_ERR_DATA, "open label listed twice");
+    c->qubit_of[l] = q;
+  }
+  for (auto& kv : c->count_of)
+    if (!c->qubit_of.count(kv.first) && kv.second != 2)
+      return fail(TN_ERR_DATA, "closed label " + std::to_string(kv.first) + " appears " +
+                                   std::to_string(kv.second) + " times (must be 2)");
+  c->packed.clear();
+  if (!samples) {
+    if (n_open > 24) return fail(TN_ERR_DATA, "full-state output limited to n_open <= 24");
+    c->full_state = true;
+    c->n_samples = n_open > 0 ? (int64_t(1) << n_open) : 1;
+    for (int64_t s = 0; s < c->n_samples; ++s) c->packed.push_back((uint64_t)s);
+  } else {
+    if (n_samples < 1) return fail(TN_ERR_DATA, "n_samples must be >= 1");
+    c->full_state = false;
+    c->n_samples = n_samples;
+    c->packed.resize(n_samples);
+    for (int64_t s = 0; s < n_samples; ++s) {
+      uint64_t v = 0;
+      for (int q = 0; q < n_open; ++q) {
+        const uint8_t b = samples[s * n_open + q];
+        if (b > 1) return fail(TN_ERR_DATA, "sample bytes must be 0 or 1");
+        v = (v << 1) | b;
+      }
+      c->packed[s] = v;
+    }
+  }
+  tn_status st = build_leaves(c);
+  if (st) return st;
+  if (c->host_only) {
+    c->leaf_absmax.assign(c->n_tensors, 0.f);
+    c->loaded = true;
+    return TN_OK;
+  }
+  if (c->d_leaf) { cudaFree(c->d_leaf); c->d_leaf = nullptr; }
+  if (c->h_leaf_pinned) { cudaFreeHost(c->h_leaf_pinned); c->h_leaf_pinned = nullptr; }
+  st = upload_leaves(c, data);
+  if (st) return st;
+  c->loaded = true;
+  return TN_OK;
+}
+
+tn_status tn_upload_tensors(tn_ctx* c, const double* data) {
+  if (!c || !c->loaded) return fail(TN_ERR_USAGE, "load a network first");
+  if (c->host_only) return fail(TN_ERR_USAGE, "host-only context (device -1) cannot execute");
+  if (!data) return fail(TN_ERR_USAGE, "data is NULL");
+  return upload_leaves(c, data);
+}
+
+tn_status tn_set_path(tn_ctx* c, int32_t n_steps, const int32_t* pairs) {
+  if (!c || !c->loaded) return fail(TN_ERR_USAGE, "load a network first");
+  free_dev(c);
+  c->pathed = false;
+  if (n_steps != c->n_tensors - 1)
+    return fail(TN_ERR_DATA, "path must have N-1 = " + std::to_string(c->n_tensors - 1) + " steps");
+  std::vector<char> alive(c->n_tensors, 1);
+  c->path.clear();
+  for (int s = 0; s < n_steps; ++s) {
+    const int i = pairs[2 * s], j = pairs[2 * s + 1];
+    if (i < 0 || j < 0 || i >= c->n_tensors || j >= c->n_tensors || i == j || !alive[i] || !alive[j])
+      return fail(TN_ERR_DATA, "path step " + std::to_string(s) + " (" + std::to_string(i) + "," +
+                                   std::to_string(j) + ") references a retired or unknown id");
+    alive[j] = 0;
+    c->path.push_back({i, j});
+  }
+  c->pathed = true;
+  return TN_OK;
+}
+
+tn_status tn_set_slices(tn_ctx* c, int32_t n_sliced, const int64_t* sliced_labels, int64_t* n_slices_out) {
+  if (!c || !c->pathed) return fail(TN_ERR_USAGE, "call tn_set_path first");
+  if (!c->host_only) TN_CUDA(cudaSetDevice(c->device));
+  std::unordered_set<int64_t> seen;
+  c->sliced.clear();
+  c->n_slices = 1;
+  for (int p = 0; p < n_sliced; ++p) {
+    const int64_t l = sliced_labels[p];
+    if (!c->dim_of.count(l)) return fail(TN_ERR_DATA, "unknown sliced label " + std::to_string(l));
+    if (c->qubit_of.count(l)) return fail(TN_ERR_DATA, "open label " + std::to_string(l) + " cannot be sliced");
+    if (!seen.insert(l).second) return fail(TN_ERR_DATA, "sliced label repeated");
+    c->sliced.push_back(l);
+    if (c->n_slices > INT64_MAX / c->dim_of[l]) return fail(TN_ERR_DATA, "too many slices");
+    c->n_slices *= c->dim_of[l];
+  }
+  tn_status st = build_plan(c);
+  if (st) { free_dev(c); return st; }
+  if (n_slices_out) *n_slices_out = c->n_slices;
+  return TN_OK;
+}
+
+tn_status tn_contract(tn_ctx* c, int64_t b, int64_t e, tn_precision prec, int32_t topk) {
+  tn_status st = check_planned(c);
+  if (st) return st;
+  if (b < 0 || e > c->n_slices || b > e)
+    return fail(TN_ERR_DATA, "slice range [" + std::to_string(b) + "," + std::to_string(e) +
+                                 ") outside [0," + std::to_string(c->n_slices) + ")");
+  if (prec != TN_PREC_EXTENDED && prec != TN_PREC_MIXED) return fail(TN_ERR_USAGE, "bad precision");
+  TN_CUDA(cudaSetDevice(c->device));
+  return run_slices(c, b, e, prec, topk);
+}
+
+tn_status tn_reset_accumulator(tn_ctx* c) {
+  tn_status st = check_planned(c);
+  if (st) return st;
+  TN_CUDA(cudaMemsetAsync(c->d_acc, 0, c->acc_elems * sizeof(double2), c->stream));
+  return TN_OK;
+}
+
+tn_status tn_sum_slices(tn_ctx* c, double* out, int64_t n_out) {
+  tn_status st = check_planned(c);
+  if (st) return st;
+  if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
+  if (!out) return fail(TN_ERR_USAGE, "out is NULL");
+  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, reinterpret_cast<double2*>(out), n_out, c->stream));
+  return TN_OK;
+}
+
+tn_status tn_sum_slices_host(tn_ctx* c, double* out_host, int64_t n_out) {
+  tn_status st = check_planned(c);
+  if (st) return st;
+  if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
+  double2* tmp = nullptr;
+  TN_CUDA(cudaMallocAsync(&tmp, n_out * sizeof(double2), c->stream));
+  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, tmp, n_out, c->stream));
+  TN_CUDA(cudaMemcpyAsync(out_host, tmp, n_out * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  TN_CUDA(cudaFreeAsync(tmp, c->stream));
+  TN_CUDA(cudaStreamSynchronize(c->stream));
+  return TN_OK;
+}
+
+tn_status tn_get_info(tn_ctx* c, tn_info* info) {
+  tn_status st = check_planned(c, false);
+  if (st) return st;
+  info->n_slices = c->n_slices;
+  info->n_out = c->n_out;
+  info->n_steps = (int32_t)c->steps.size();
+  int ntc = 0;
+  for (auto& s : c->steps) ntc += s.tc;
+  info->n_tc_steps = ntc;
+  info->flops_per_slice = c->flops_per_slice;
+  info->tc_flops_per_slice = c->tc_flops;
+  info->bytes_per_slice = c->bytes_per_slice;
+  info->peak_elements = c->peak;
+  info->device_bytes = c->device_bytes;
+  return TN_OK;
+}
+
+tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
+  tn_status st = check_planned(c, false);
+  if (st) return st;
+  std::string o = "{\"n_slices\":" + std::to_string(c->n_slices) + ",\"sliced\":[";
+  for (size_t p = 0; p < c->sliced.size(); ++p) { if (p) o += ","; o += std::to_string(c->sliced[p]); }
+  o += "],\"steps\":[";
+  for (size_t s = 0; s < c->steps.size(); ++s) {
+    const StepPlan& sp = c->steps[s];
+    if (s) o += ",";
+    char b[512];
+    snprintf(b, sizeof(b),
+             "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
+             "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"ia\":",
+             sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
+             sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false");
+    o += b;
+    if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
+    o += ",\"ib\":";
+    if (sp.merge) json_u64_list(o, sp.ib); else o += "null";
+    o += "}";
+  }
+  o += "],\"out_pos\":";
+  json_u64_list(o, c->out_pos);
+  char b[256];
+  snprintf(b, sizeof(b), ",\"flops_per_slice\":%.17g,\"tc_flops_per_slice\":%.17g,\"peak_elements\":%.17g}",
+           c->flops_per_slice, c->tc_flops, c->peak);
+  o += b;
+  if (len) *len = o.size();
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, o.size());
+    memcpy(buf, o.data(), n);
+    buf[n] = 0;
+  }
+  return TN_OK;
+}
+
+tn_status tn_set_profiling(tn_ctx* c, int enabled) {
+  if (!c) return fail(TN_ERR_USAGE, "null context");
+  c->profiling = enabled != 0;
+  return TN_OK;
+}
+
+tn_status tn_get_kernel_stats(tn_ctx* c, int family, tn_kernel_stats* out) {
+  if (!c || family < 0 || family > 3 || !out) return fail(TN_ERR_USAGE, "bad arguments");
+  if (!c->pending.empty()) {
+    TN_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& p : c->pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      c->stats[p.family].ms += ms;
+      c->stats[p.family].flops += p.flops;
+      c->stats[p.family].bytes += p.bytes;
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    c->pending.clear();
+  }
+  out->launches = c->stats[family].launches;
+  out->ms = c->stats[family].ms;
+  out->flops = c->stats[family].flops;
+  out->bytes = c->stats[family].bytes;
+  return TN_OK;
+}
+
+tn_status tn_reset_kernel_stats(tn_ctx* c) {
+  if (!c) return fail(TN_ERR_USAGE, "null context");
+  tn_kernel_stats tmp;
+  tn_get_kernel_stats(c, 0, &tmp);
+  for (auto& s : c->stats) s = KStats();
+  return TN_OK;
+}
+
+tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t J, int64_t m, int64_t n,
+                   int64_t k, int64_t ga, int64_t gb, const int32_t* ia, const int32_t* ib, int passes,
+                   int force_simt) {
+  if (!c) return fail(TN_ERR_USAGE, "null context");
+  if (c->host_only) return fail(TN_ERR_USAGE, "host-only context (device -1) cannot execute");
+  if (J < 1 || m < 1 || n < 1 || k < 1 || ga < 1 || gb < 1) return fail(TN_ERR_USAGE, "bad sizes");
+  if (passes != 1 && passes != 3) return fail(TN_ERR_USAGE, "passes must be 1 or 3");
+  TN_CUDA(cudaSetDevice(c->device));
+  cudaStream_t sm = c->stream;
+  unsigned* am = nullptr;
+  int* sc = nullptr;
+  TN_CUDA(cudaMalloc(&am, 16));
+  TN_CUDA(cudaMalloc(&sc, 16));
+  TN_CUDA(cudaMemsetAsync(am, 0, 16, sm));
+  const float2* A2 = reinterpret_cast<const float2*>(A);
+  const float2* B2 = reinterpret_cast<const float2*>(B);
+  TN_CUDA(tn::launch_absmax(A2, ga * m * k, am, sm));
+  TN_CUDA(tn::launch_absmax(B2, gb * n * k, am + 1, sm));
+  tn_status result = TN_OK;
+  if (force_simt) {
+    tn::EinsumDesc e;
+    memset(&e, 0, sizeof(e));
+    e.A = A2; e.B = B2; e.C = reinterpret_cast<float2*>(C);
+    e.a_leaf = e.b_leaf = -1;
+    e.J = J; e.ia = ia; e.ib = ib; e.a_gs = m * k; e.b_gs = n * k;
+    e.M = m; e.N = n; e.K = k;
+    e.nm = 1; e.m_ext[0] = m; e.m_sa[0] = k;
+    e.nn = 1; e.n_ext[0] = n; e.n_sb[0] = k;
+    e.nk = 1; e.k_ext[0] = k; e.k_sa[0] = 1; e.k_sb[0] = 1;
+    tn::EinsumDesc* d = nullptr;
+    TN_CUDA(cudaMalloc(&d, sizeof(e)));
+    TN_CUDA(cudaMemcpyAsync(d, &e, sizeof(e), cudaMemcpyHostToDevice, sm));
+    TN_CUDA(tn::launch_einsum(d, J * m * n, nullptr, sm));
+    TN_CUDA(cudaStreamSynchronize(sm));
+    cudaFree(d);
+  } else {
+    const int64_t Kpad = (k + 7) / 8 * 8;
+    const int64_t b0 = (4 * ga * m * Kpad * 2 + 1023) / 1024 * 1024;
+    const int64_t b1 = (4 * gb * n * Kpad * 2 + 1023) / 1024 * 1024;
+    uint8_t* scr = nullptr;
+    TN_CUDA(cudaMalloc(&scr, b0 + b1));
+    tn::PrepDesc p[2];
+    tn::GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    char err[256];
+    for (int side = 0; side < 2; ++side) {
+      memset(&p[side], 0, sizeof(tn::PrepDesc));
+      const int64_t R = side ? n : m, G = side ? gb : ga;
+      p[side].src = side ? B2 : A2;
+      p[side].leaf = -1;
+      p[side].G = G; p[side].R = R; p[side].K = k; p[side].Kpad = Kpad;
+      p[side].g_stride = R * k;
+      p[side].nr = 1; p[side].r_ext[0] = R; p[side].r_s[0] = k;
+      p[side].nk = 1; p[side].k_ext[0] = k; p[side].k_s[0] = 1;
+      p[side].dst = reinterpret_cast<__half*>(scr + (side ? b0 : 0));
+      p[side].plane_elems = G * R * Kpad;
+      p[side].absmax_in = am + side;
+      p[side].scale_out = sc + side;
+      if (!tn::encode_plane_map(side ? &g.mapB : &g.mapA, p[side].dst, Kpad, R, G, 4, 128, err, sizeof(err))) {
+        cudaFree(scr);
+        return fail(TN_ERR_INTERNAL, err);
+      }
+    }
+    tn::PrepDesc* dp = nullptr;
+    TN_CUDA(cudaMalloc(&dp, sizeof(p)));
+    TN_CUDA(cudaMemcpyAsync(dp, p, sizeof(p), cudaMemcpyHostToDevice, sm));
+    const int planes = passes == 3 ? 4 : 2;
+    TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, nullptr, sm));
+    TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, nullptr, sm));
+    g.J = (int32_t)J; g.M = (int32_t)m; g.N = (int32_t)n; g.K = (int32_t)k;
+    g.ia = ia; g.ib = ib;
+    g.C = reinterpret_cast<float2*>(C);
+    g.scaleA = sc; g.scaleB = sc + 1;
+    g.absmax_out = nullptr; g.acc = nullptr;
+    g.tiles_m = (int32_t)((m + 127) / 128);
+    g.tiles_n = (int32_t)((n + 127) / 128);
+    g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * J;
+    TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));
+    cudaError_t e = cudaStreamSynchronize(sm);
+    cudaFree(dp);
+    cudaFree(scr);
+    if (e != cudaSuccess) result = fail(TN_ERR_CUDA, std::string("cgemm: ") + cudaGetErrorString(e));
+  }
+  cudaFree(am);
+  cudaFree(sc);
+  return result;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// Internal descriptors shared by the host planner and the sm_100a kernels.
+// Device descriptors live in device memory (uploaded once per plan) so the
+// per-slice launch sequence only passes pointers.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#define TN_MAXD 40          // max coalesced dims per operand side after merging runs
+
+namespace tn {
+
+// ---------------------------------------------------------------- SIMT einsum
+// C[j][m][n] (+)= Σ_k A[slabA(j), m, k] · B[slabB(j), n, k] over strided views.
+struct EinsumDesc {
+  const float2* A; const float2* B; float2* C;
+  int64_t a_off, b_off;           // static element offsets
+  int32_t a_leaf, b_leaf;         // index into the per-slice leaf offset array, or -1
+  int64_t J;                      // batch (merged sparse configurations)
+  const int32_t* ia; const int32_t* ib;   // slab tables (nullable -> slab 0)
+  int64_t a_gs, b_gs;             // slab strides (elements)
+  int64_t M, N, K;
+  int32_t nm, nn, nk;
+  int64_t m_ext[TN_MAXD], m_sa[TN_MAXD];
+  int64_t n_ext[TN_MAXD], n_sb[TN_MAXD];
+  int64_t k_ext[TN_MAXD], k_sa[TN_MAXD], k_sb[TN_MAXD];
+  unsigned* absmax_out;           // nullable: atomicMax of |re|,|im| bits
+  double2* acc;                   // nullable: acc[idx] += C instead of storing C
+};
+
+// ---------------------------------------------------------------- operand prep
+// Permute a strided complex64 view into K-contiguous fp16 planes with a
+// per-tensor power-of-two scale: plane p of element (g, r, k) at
+// dst[p*plane_elems + (g*R + r)*Kpad + k]; planes = re_hi, im_hi[, re_lo, im_lo].
+struct PrepDesc {
+  const float2* src; int64_t off; int32_t leaf;
+  int64_t G, R, K, Kpad, g_stride;
+  int32_t nr, nk;
+  int64_t r_ext[TN_MAXD], r_s[TN_MAXD];
+  int64_t k_ext[TN_MAXD], k_s[TN_MAXD];
+  __half* dst; int64_t plane_elems;
+  const unsigned* absmax_in;      // absmax of the source tensor (float bits)
+  int* scale_out;                 // receives the exponent s (x * 2^s is split)
+};
+
+// ---------------------------------------------------------------- tcgen05 GEMM
+struct GemmArgs {
+  CUtensorMap mapA;               // 4D fp16 (Kpad, R, G, planes), box (32, 128, 1, 1), SW64
+  CUtensorMap mapB;
+  int32_t J, M, N, K;             // M = rows of A operand, N = rows of B operand (complex)
+  const int32_t* ia; const int32_t* ib;
+  float2* C;                      // [J][M][N] complex64
+  const int* scaleA; const int* scaleB;
+  unsigned* absmax_out;
+  double2* acc;                   // nullable: fused fp64 slice-accumulate
+  int32_t tiles_m, tiles_n;
+  int64_t n_tiles;
+};
+
+// ---------------------------------------------------------------- slice select
+struct SliceDesc {
+  int32_t n_sliced;
+  int64_t dims[64];
+  int32_t n_terms;                // (leaf, sliced index, stride) terms
+  const int32_t* term_leaf; const int32_t* term_p; const int64_t* term_stride;
+  int32_t n_leaves;
+  int64_t* leaf_off;              // out: per-leaf dynamic element offset
+  int64_t* counter;               // in/out: current slice index (incremented)
+  unsigned* absmax; int32_t absmax_first, absmax_count;  // zeroed per slice
+};
+
+// kernel launchers (kernels.cu / gemm_tcgen05.cu)
+cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes,
+                        const int64_t* leaf_off, cudaStream_t s);
+cudaError_t launch_einsum(const EinsumDesc* d_desc, int64_t total, const int64_t* leaf_off,
+                          cudaStream_t s);
+cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
+                              cudaStream_t s);
+cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);
+cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s);
+bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
+                      int planes, int box_rows, char* err, size_t errcap);
+
+}  // namespace tn

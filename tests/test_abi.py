@@ -1,0 +1,119 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/tn.h
+declares, and its host-side planner (path replay, Eq. 3 set rule, Eq. 4/5
+bookkeeping, Eq. 7 merge tables, slice validation) agrees bit-exactly with the
+oracle's independent derivation.  No GPU needed (host-only context, device -1)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from tnworkloads import configs, grid_layout, random_circuit, circuit_to_network, greedy_path
+from tnworkloads.paths import slice_greedy
+from paper_2310_03978_b200 import tn as tnlib
+from paper_2310_03978_b200 import Contraction, TNError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tn.h")).read()
+    return sorted(set(re.findall(r"^TN_API\s+[\w\s\*]+?\b(tn_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = tnlib.lib()
+    declared = header_symbols()
+    assert len(declared) >= 15
+    for s in declared:
+        assert hasattr(L, s), s
+    assert sorted(tnlib.SYMBOLS) == declared
+    assert b"sm_100a" in L.tn_version()
+
+
+def _check_plan(w):
+    c = Contraction(device=-1)
+    ns = c.setup(w.net, w.samples, w.path, w.sliced)
+    assert ns == w.n_slices
+    pj = c.plan_json()
+    bk = oracle.plan_bookkeeping(w.net, w.path, w.sliced, w.samples)
+    assert len(pj["steps"]) == len(bk)
+    for a, b in zip(pj["steps"], bk):
+        for key in ["i", "j", "J", "m", "n", "k", "tcc", "tmc"]:
+            assert a[key] == b[key], (key, a, b)
+        assert a["ia"] == b["ia"] and a["ib"] == b["ib"]
+    info = c.info()
+    assert info["flops_per_slice"] == sum(r["tcc"] for r in bk)
+    return c, pj
+
+
+@pytest.mark.parametrize("mode", ["sparse", "full", "single", "subspace"])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_plan_bookkeeping_matches_oracle(mode, seed):
+    w = configs.small(grid=(3, 3), cycles=6, mode=mode, n_samples=24, n_slices=4, seed=seed)
+    _check_plan(w)
+
+
+def test_plan_bookkeeping_raw_network_and_output_positions():
+    w = configs.small(grid=(2, 4), cycles=5, mode="sparse", n_samples=40, n_slices=2, seed=3,
+                      simplify=False)
+    c, pj = _check_plan(w)
+    # a9: root table is sorted unique samples; out_pos maps caller order onto it
+    s = w.samples.astype(np.int64)
+    packed = (s << (s.shape[1] - 1 - np.arange(s.shape[1]))[None, :]).sum(1)
+    uniq = np.unique(packed)
+    assert pj["out_pos"] == [int(np.searchsorted(uniq, v)) for v in packed]
+
+
+def test_c2_plan_matches_oracle_bookkeeping():
+    w = configs.c2()
+    c, pj = _check_plan(w)
+    assert c.info()["n_slices"] == 64
+    assert c.info()["n_out"] == 1024
+
+
+def test_error_codes():
+    w = configs.small(grid=(2, 3), cycles=4, mode="sparse", n_samples=8, n_slices=1, seed=5)
+    ranks, labels, dims, data, opens = w.net.flat()
+    c = Contraction(device=-1)
+    with pytest.raises(TNError) as e:
+        c.set_path(w.path)                       # wrong call order
+    assert e.value.status == 1
+    c.load_network(ranks, labels, dims, data, opens, w.samples)
+    bad = list(w.path)
+    bad[1] = (bad[0][1], bad[1][1])              # references a retired id
+    with pytest.raises(TNError) as e:
+        c.set_path(bad)
+    assert e.value.status == 2
+    with pytest.raises(TNError) as e:
+        c.set_path(w.path[:-1])                  # not N-1 steps
+    assert e.value.status == 2
+    c.set_path(w.path)
+    with pytest.raises(TNError) as e:
+        c.set_slices([opens[0]])                 # open bond cannot be sliced
+    assert e.value.status == 2
+    closed = [x for x in labels if x not in set(opens)]
+    with pytest.raises(TNError) as e:
+        c.set_slices([closed[0], closed[0]])     # repeated
+    assert e.value.status == 2
+    with pytest.raises(TNError) as e:
+        c.set_slices([10 ** 9])                  # unknown
+    assert e.value.status == 2
+    assert c.set_slices([closed[0]]) == 2
+    with pytest.raises(TNError) as e:
+        c.contract(0, 1)                         # host-only context cannot execute
+    assert e.value.status == 1
+    # malformed networks
+    c2 = Contraction(device=-1)
+    lab2 = labels.copy()
+    lab2[0] = lab2[1] if ranks[0] > 1 else lab2[0]
+    if ranks[0] > 1:
+        with pytest.raises(TNError) as e:        # label repeated inside a tensor
+            c2.load_network(ranks, lab2, dims, data, opens, w.samples)
+        assert e.value.status == 2
+    smp = w.samples.copy()
+    smp[0, 0] = 2
+    with pytest.raises(TNError) as e:
+        c2.load_network(ranks, labels, dims, data, opens, smp)
+    assert e.value.status == 2

@@ -1,0 +1,204 @@
+"""GPU parity tests (``-m gpu``): the CUDA path, called through the C ABI, against
+the CPU fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): relative L2 over the amplitude vector
+<= 1e-5 for the extended path, <= 5e-3 for the mixed path; bookkeeping and
+slice indexing bit-exact.  Kernel unit tests compare the tcgen05 complex GEMM
+with an fp64 numpy product of the same complex64 inputs; their tolerances are
+derived in DESIGN.md §Tolerances (3-pass split: a few 2^-22 per product plus
+fp32 accumulation; 1-pass: fp16 rounding 2^-11 per operand).
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle                                          # noqa: E402
+from tnworkloads import configs, gate_matrix           # noqa: E402
+from paper_2310_03978_b200 import Contraction          # noqa: E402
+
+EXT_TOL = 1e-5
+MIX_TOL = 5e-3
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    yield c
+    c.close()
+
+
+@pytest.fixture
+def force_tc(monkeypatch):
+    """Route small steps to the tcgen05 GEMM so parity tests exercise it with
+    several tiles and ragged tails (thresholds are read at plan time)."""
+    monkeypatch.setenv("TN_TC_MIN_BIG", "8")
+    monkeypatch.setenv("TN_TC_MIN_SMALL", "2")
+    monkeypatch.setenv("TN_TC_MIN_K", "2")
+
+
+def crandn(rng, *shape):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64)
+
+
+# ----------------------------------------------------------------------------- a4 / a5 kernels
+
+@pytest.mark.parametrize("J,m,n,k,ga,gb", [
+    (1, 128, 128, 32, 1, 1),      # one tile, one k-block
+    (1, 300, 200, 100, 1, 1),     # ragged M, N, K tails, several tiles
+    (1, 1024, 512, 2048, 1, 1),   # many tiles, deep K
+    (5, 130, 70, 48, 3, 4),       # gather-batched (sparse einsum), tables
+    (1, 256, 16, 8, 1, 1),        # narrow N, K < BK
+])
+@pytest.mark.parametrize("passes", [3, 1])
+def test_cgemm_tcgen05_vs_fp64(ctx, J, m, n, k, ga, gb, passes):
+    rng = np.random.default_rng(J * 1000 + m + n + k)
+    A = crandn(rng, ga, m, k)
+    B = crandn(rng, gb, n, k)
+    ia = rng.integers(0, ga, J).astype(np.int32)
+    ib = rng.integers(0, gb, J).astype(np.int32)
+    ref = np.einsum("jmk,jnk->jmn", A[ia].astype(np.complex128), B[ib].astype(np.complex128))
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.zeros((J, m, n), dtype=torch.complex64, device="cuda")
+    dia, dib = torch.from_numpy(ia).cuda(), torch.from_numpy(ib).cuda()
+    ctx.cgemm(dA, dB, dC, J, m, n, k, ga, gb, dia, dib, passes=passes)
+    out = dC.cpu().numpy()
+    err = rel_l2(out, ref)
+    bound = 2e-6 if passes == 3 else 2e-3
+    assert err < bound, err
+
+
+def test_cgemm_simt_vs_fp64(ctx):
+    rng = np.random.default_rng(7)
+    J, m, n, k, ga, gb = 3, 37, 29, 41, 2, 3
+    A, B = crandn(rng, ga, m, k), crandn(rng, gb, n, k)
+    ia = np.array([1, 0, 1], np.int32)
+    ib = np.array([2, 2, 0], np.int32)
+    ref = np.einsum("jmk,jnk->jmn", A[ia].astype(np.complex128), B[ib].astype(np.complex128))
+    dC = torch.zeros((J, m, n), dtype=torch.complex64, device="cuda")
+    ctx.cgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), dC, J, m, n, k, ga, gb,
+              torch.from_numpy(ia).cuda(), torch.from_numpy(ib).cuda(), force_simt=True)
+    assert rel_l2(dC.cpu().numpy(), ref) < 1e-6
+
+
+def test_cgemm_exact_small_integers(ctx):
+    """Integer-valued operands: every product and partial sum is exact in fp32,
+    so the tensor-core result must be bit-exact (checks operand mapping, the
+    negate bit and the re/im wiring independently of rounding)."""
+    rng = np.random.default_rng(11)
+    m, n, k = 192, 160, 96
+    A = (rng.integers(-8, 9, (1, m, k)) + 1j * rng.integers(-8, 9, (1, m, k))).astype(np.complex64)
+    B = (rng.integers(-8, 9, (1, n, k)) + 1j * rng.integers(-8, 9, (1, n, k))).astype(np.complex64)
+    ref = np.einsum("jmk,jnk->jmn", A.astype(np.complex128), B.astype(np.complex128))
+    for passes in (1, 3):
+        dC = torch.zeros((1, m, n), dtype=torch.complex64, device="cuda")
+        ctx.cgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), dC, 1, m, n, k,
+                  passes=passes)
+        assert np.array_equal(dC.cpu().numpy().astype(np.complex128), ref)
+
+
+# ----------------------------------------------------------------------------- whole contractions
+
+def run_gpu(ctx, w, precision="extended", topk=10, slices=None):
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(w.net, w.samples, w.path, w.sliced)
+    b, e = (0, c.n_slices) if slices is None else slices
+    c.contract(b, e, precision=precision, mixed_topk=topk)
+    out = c.sum_slices_host()
+    info = c.info()
+    c.close()
+    return out, info
+
+
+@pytest.mark.parametrize("mode", ["sparse", "full", "single", "subspace"])
+@pytest.mark.parametrize("tc", [False, True])
+def test_contraction_vs_oracle(ctx, mode, tc, monkeypatch):
+    if tc:
+        monkeypatch.setenv("TN_TC_MIN_BIG", "8")
+        monkeypatch.setenv("TN_TC_MIN_SMALL", "2")
+        monkeypatch.setenv("TN_TC_MIN_K", "2")
+    w = configs.small(grid=(3, 4), cycles=8, mode=mode, n_samples=64, n_slices=8, seed=2)
+    ref = oracle.contract(w.net, w.path, w.sliced, w.samples)
+    out, info = run_gpu(ctx, w)
+    if tc:
+        assert info["n_tc_steps"] > 0
+    assert rel_l2(out, ref) <= EXT_TOL
+    out_m, _ = run_gpu(ctx, w, precision="mixed", topk=10)
+    assert rel_l2(out_m, ref) <= MIX_TOL
+
+
+def test_per_slice_parity_and_accumulation(ctx, force_tc):
+    w = configs.small(grid=(3, 3), cycles=7, mode="sparse", n_samples=32, n_slices=8, seed=4)
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(w.net, w.samples, w.path, w.sliced)
+    acc = np.zeros(c.n_out, complex)
+    for t in [0, 3, 7]:
+        c.reset_accumulator()
+        c.contract(t, t + 1)
+        got = c.sum_slices_host()
+        ref = oracle.contract_slice(w.net, w.path, w.sliced, t, w.samples)
+        assert rel_l2(got, ref) <= EXT_TOL
+    # accumulation over disjoint ranges == the full sum
+    c.reset_accumulator()
+    c.contract(0, 5)
+    c.contract(5, 8)
+    assert rel_l2(c.sum_slices_host(), oracle.contract(w.net, w.path, w.sliced, w.samples)) <= EXT_TOL
+    c.close()
+
+
+def test_c1_vs_statevector(ctx):
+    for mode in ["single", "full"]:
+        w = configs.c1(mode)
+        psi = oracle.statevector(w.circuit, gate_matrix)
+        ref = oracle.amplitudes_for(psi, w.samples)
+        out, _ = run_gpu(ctx, w)
+        assert rel_l2(out, ref) <= EXT_TOL
+        if mode == "full":
+            assert abs(np.sum(np.abs(out) ** 2) - 1) < 1e-5
+
+
+def test_echo_exact(ctx, force_tc):
+    from tnworkloads import grid_layout
+    w = configs.echo(grid_layout(3, 4), 4, seed=41, mode="sparse", n_samples=16, n_slices=4)
+    out, _ = run_gpu(ctx, w)
+    is0 = ~w.samples.any(axis=1)
+    assert np.abs(out[is0] - 1).max() < 1e-5
+    assert np.abs(out[~is0]).max() < 1e-5
+
+
+def test_c2_sampled_slices_at_full_size(ctx):
+    """C2 at full size (30 q, 2^10 amplitudes, the 64-slice plan the bench times):
+    a GPU slice equals the sum of its GPU sub-slices (slicing identity, any size),
+    and sub-slices are compared element by element with the oracle."""
+    w = configs.c2()
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(w.net, w.samples, w.path, w.sliced)
+    c.contract(5, 6)
+    slice5 = c.sum_slices_host()
+    c.close()
+    # refine: slice 6 more bonds -> 64 sub-slices per coarse slice
+    from tnworkloads.paths import slice_greedy
+    extra, _ = slice_greedy(w.net, w.samples, w.path, n_slices=64 * 64)
+    extra = [x for x in extra if x not in w.sliced]
+    fine = list(w.sliced) + extra[: 6]
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    nfine = c.setup(w.net, w.samples, w.path, fine)
+    per = nfine // 64
+    c.contract(5 * per, 6 * per)
+    sub_sum = c.sum_slices_host()
+    assert rel_l2(sub_sum, slice5) <= 1e-5
+    for t in [5 * per, 5 * per + per // 2]:
+        c.reset_accumulator()
+        c.contract(t, t + 1)
+        got = c.sum_slices_host()
+        ref = oracle.contract_slice(w.net, w.path, fine, t, w.samples)
+        assert rel_l2(got, ref) <= EXT_TOL
+    c.close()
