@@ -11,24 +11,34 @@
 // Extended precision (3 passes) follows Eq. 8 with fp16
 // in place of tf32 (the 3xFP16 variant, L383-386): per real product
 //   x·y ≈ x_big·y_small + x_small·y_big + x_big·y_big   (small·small dropped,
-// small terms issued first), all accumulating in the fp32 TMEM accumulator.
-// Mixed mode (1 pass) keeps only big·big (L411, L442).
+// small terms issued first).  Mixed mode (1 pass) keeps only big·big (L442).
+//
+// Accumulator promotion.  tcgen05 kind::f16 truncates (RZ) its fp32 TMEM
+// accumulator after every MMA (measured: tools/accum_probe.py, DESIGN.md
+// "Numerics").  A truncating chain of T MMAs biases the result toward zero by
+// ≈0.37·2^-24·T relative, so a K-loop of thousands of MMAs drifts by 1e-5..1e-3.
+// The MMA warp therefore restarts the TMEM accumulator every `kchunk` k-blocks
+// and the epilogue warps add each finished chunk into an fp32 register sum with
+// round-to-nearest: the bias becomes ≈0.37·2^-24·(MMAs per chunk) independently
+// of K, and the chunk sums combine without bias.
 //
 // Sparse einsum (Eq. 7) is the same kernel: batch j selects the A and
 // B slabs through the gather tables ia/ib — the "separate pointers for each
 // matrix of the batched GEMM" of L354 become TMA slab coordinates, so no
 // gathered copies are materialised.
 //
-// Structure (one CTA per SM, persistent, 6 warps):
+// Structure (one CTA per SM, persistent, 10 warps):
 //   warp 0      TMA producer: 4D tensor-map loads (K, rows, slab, plane), box
 //               32x128, SWIZZLE_64B, into a STAGES-deep smem ring (mbarrier tx).
 //   warp 1      TMEM allocator (512 cols) + single-thread tcgen05.mma issuer,
-//               kind::f16, M=128 N=128 K=16, accumulators Cr|Ci = 256 TMEM
-//               columns, double-buffered across tiles; tcgen05.commit frees
-//               smem stages and hands full accumulators to the epilogue.
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> scale by 2^-(sA+sB) ->
-//               float2 stores of C (or fused fp64 accumulate into the slice sum)
-//               + absmax of the result for the consumer's rescale.
+//               kind::f16, M=128 N=128 K=16; a chunk accumulator Cr|Ci is 256
+//               TMEM columns, double-buffered; tcgen05.commit frees smem stages
+//               and hands finished chunks to the epilogue.
+//   warps 2-9   epilogue: warp (quadrant q, half h) owns TMEM lanes 32q..32q+31
+//               and output columns 64h..64h+63 of both Cr and Ci; tcgen05.ld
+//               32x32b.x32 -> fp32 RN register sums -> at tile end scale by
+//               2^-(sA+sB) and store complex64 (or fused fp64 accumulate into the
+//               slice sum, a8) + absmax of the result for the consumer's rescale.
 #include "tn_internal.h"
 #include <cstdio>
 
@@ -37,7 +47,8 @@ namespace {
 
 constexpr int BM = 128, BN = 128, BK = 32;          // BK in complex k (64 B fp16 rows)
 constexpr int PLANE_TILE = 128 * BK * 2;            // 8 KiB per plane tile
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr uint32_t TMEM_COLS = 512;
 
 template <int PASSES>
@@ -137,12 +148,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = empty + STAGES;     // chunk accumulator ready (MMA -> epilogue)
+  uint64_t* cempty = cfull + 2;         // chunk accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int kblocks = (args.K + BK - 1) / BK;
+  const int kchunk = (args.kchunk > 0 && args.kchunk < kblocks) ? args.kchunk : kblocks;
+  const int nchunks = (kblocks + kchunk - 1) / kchunk;
+  const int64_t per_j = (int64_t)args.tiles_m * args.tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -150,8 +165,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], NUM_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapA)) : "memory");
@@ -167,9 +182,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const int kblocks = (args.K + BK - 1) / BK;
-  const int64_t per_j = (int64_t)args.tiles_m * args.tiles_n;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -205,14 +217,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
       // ---------------------------------------------------------------- MMA issuer
       int stage = 0;
       uint32_t phase = 0;
-      int as = 0;
-      uint32_t aphase = 0;
+      int cb = 0;
+      uint32_t cphase = 0;
       for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[as], aphase ^ 1);
-        fence_after();
-        const uint32_t d_re = tmem_base + as * 256;
-        const uint32_t d_im = d_re + 128;
         for (int kb = 0; kb < kblocks; ++kb) {
+          const int kin = kb % kchunk;
+          if (kin == 0) {
+            mbar_wait(&cempty[cb], cphase ^ 1);     // chunk buffer drained by the epilogue
+            fence_after();
+          }
+          const uint32_t d_re = tmem_base + cb * 256;
+          const uint32_t d_im = d_re + 128;
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint32_t st = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -223,7 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
             const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
             const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
             const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
-            const uint32_t acc0 = (kb | kk) != 0;
+            const uint32_t acc0 = (kin | kk) != 0;
             if (PASSES == 3) {
               const uint64_t arl = sdesc(st + 2 * PLANE_TILE + koff);
               const uint64_t ail = sdesc(st + 3 * PLANE_TILE + koff);
@@ -255,75 +270,91 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
             stage = 0;
             phase ^= 1;
           }
-        }
-        mma_commit(&tfull[as]);        // accumulator ready for the epilogue
-        if (++as == 2) {
-          as = 0;
-          aphase ^= 1;
+          if (kin == kchunk - 1 || kb == kblocks - 1) {
+            mma_commit(&cfull[cb]);    // chunk accumulator ready for the epilogue
+            if (++cb == 2) {
+              cb = 0;
+              cphase ^= 1;
+            }
+          }
         }
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    // ---------------------------------------------------------------- epilogue (warps 2..9)
     const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;           // output columns 64*half .. 64*half+63
     const int row = quad * 32 + lane;
     const float scale = ldexpf(1.0f, -(*args.scaleA + *args.scaleB));
-    const bool vec_ok = (args.N % 2) == 0;
     float amax = 0.f;
-    int as = 0;
-    uint32_t aphase = 0;
+    int cb = 0;
+    uint32_t cphase = 0;
     for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
       const int j = (int)(tile / per_j);
       const int rem = (int)(tile % per_j);
       const int mt = rem / args.tiles_n, nt = rem % args.tiles_n;
-      mbar_wait(&tfull[as], aphase);
-      fence_after();
+      float sr[64], si[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) { sr[i] = 0.f; si[i] = 0.f; }
+      for (int ch = 0; ch < nchunks; ++ch) {
+        mbar_wait(&cfull[cb], cphase);
+        fence_after();
+        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + cb * 256 + half * 64;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t vr[32], vi[32];
+          TN_LD32(vr, tb + c * 32);
+          TN_LD32(vi, tb + 128 + c * 32);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {     // fp32 round-to-nearest promotion of the chunk
+            sr[c * 32 + i] += __uint_as_float(vr[i]);
+            si[c * 32 + i] += __uint_as_float(vi[i]);
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[cb]);
+        if (++cb == 2) {
+          cb = 0;
+          cphase ^= 1;
+        }
+      }
       const int m = mt * BM + row;
-      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + as * 256;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t vr[32], vi[32];
-        TN_LD32(vr, tbase + c * 32);
-        TN_LD32(vi, tbase + 128 + c * 32);
-        tmem_wait_ld();
-        const int n0 = nt * BN + c * 32;
-        if (m < args.M && n0 < args.N) {
-          const int64_t base = ((int64_t)j * args.M + m) * (int64_t)args.N + n0;
-          const int cnt = min(32, args.N - n0);
-          if (args.acc) {
-            for (int i = 0; i < cnt; ++i) {
-              const float re = __uint_as_float(vr[i]) * scale, im = __uint_as_float(vi[i]) * scale;
+      const int n0 = nt * BN + half * 64;
+      if (m < args.M && n0 < args.N) {
+        const int64_t base = ((int64_t)j * args.M + m) * (int64_t)args.N + n0;
+        if (args.acc) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            if (n0 + i < args.N) {
+              const float re = sr[i] * scale, im = si[i] * scale;
               double2 o = args.acc[base + i];
               o.x += (double)re;
               o.y += (double)im;
               args.acc[base + i] = o;
               amax = fmaxf(amax, fmaxf(fabsf(re), fabsf(im)));
             }
-          } else if (vec_ok && cnt == 32) {
-            float4* dst = reinterpret_cast<float4*>(args.C + base);
+          }
+        } else if ((args.N % 2) == 0 && n0 + 64 <= args.N) {
+          float4* dst = reinterpret_cast<float4*>(args.C + base);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float r0 = __uint_as_float(vr[2 * i]) * scale, i0 = __uint_as_float(vi[2 * i]) * scale;
-              const float r1 = __uint_as_float(vr[2 * i + 1]) * scale,
-                          i1 = __uint_as_float(vi[2 * i + 1]) * scale;
-              dst[i] = make_float4(r0, i0, r1, i1);
-              amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
-            }
-          } else {
-            for (int i = 0; i < cnt; ++i) {
-              const float re = __uint_as_float(vr[i]) * scale, im = __uint_as_float(vi[i]) * scale;
+          for (int i = 0; i < 32; ++i) {
+            const float r0 = sr[2 * i] * scale, i0 = si[2 * i] * scale;
+            const float r1 = sr[2 * i + 1] * scale, i1 = si[2 * i + 1] * scale;
+            dst[i] = make_float4(r0, i0, r1, i1);
+            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            if (n0 + i < args.N) {
+              const float re = sr[i] * scale, im = si[i] * scale;
               args.C[base + i] = make_float2(re, im);
               amax = fmaxf(amax, fmaxf(fabsf(re), fabsf(im)));
             }
           }
         }
-      }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
-      if (++as == 2) {
-        as = 0;
-        aphase ^= 1;
       }
     }
     if (args.absmax_out) {

@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
     for (int i = d.nm - 1; i >= 0; --i) { ao += (t % d.m_ext[i]) * d.m_sa[i]; t /= d.m_ext[i]; }
     t = n;
     for (int i = d.nn - 1; i >= 0; --i) { bo += (t % d.n_ext[i]) * d.n_sb[i]; t /= d.n_ext[i]; }
-    float cr = 0.f, ci = 0.f;
+    // fp64 accumulation: a long fp32 RN chain would cost ~2^-24·sqrt(K/2) relative
+    double cr = 0.0, ci = 0.0;
     for (int64_t ko = 0; ko < kouter; ++ko) {
       int64_t ak = ao, bk = bo, u = ko;
       for (int i = nk - 2; i >= 0; --i) {
@@ -149,21 +150,21 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
       for (int64_t ki = 0; ki < klast; ++ki) {
         const float2 a = A[ak + ki * ka_last];
         const float2 b = B[bk + ki * kb_last];
-        cr = fmaf(a.x, b.x, cr);
-        cr = fmaf(-a.y, b.y, cr);
-        ci = fmaf(a.x, b.y, ci);
-        ci = fmaf(a.y, b.x, ci);
+        cr = fma((double)a.x, (double)b.x, cr);
+        cr = fma(-(double)a.y, (double)b.y, cr);
+        ci = fma((double)a.x, (double)b.y, ci);
+        ci = fma((double)a.y, (double)b.x, ci);
       }
     }
     if (d.acc) {
       double2 o = d.acc[idx];
-      o.x += (double)cr;
-      o.y += (double)ci;
+      o.x += cr;
+      o.y += ci;
       d.acc[idx] = o;
     } else {
-      d.C[idx] = make_float2(cr, ci);
+      d.C[idx] = make_float2((float)cr, (float)ci);
     }
-    amax = fmaxf(amax, fmaxf(fabsf(cr), fabsf(ci)));
+    amax = fmaxf(amax, fmaxf(fabsf((float)cr), fabsf((float)ci)));
   }
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }

@@ -93,6 +93,8 @@ struct tn_ctx {
   bool host_only = false;   // device = -1: plan/bookkeeping only, no CUDA calls
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  // k-blocks per promoted TMEM chunk: 3-pass / 1-pass
+  int kchunk3 = 1, kchunk1 = 0;
   // network
   bool loaded = false, pathed = false, planned = false;
   int n_tensors = 0;
@@ -706,8 +708,10 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
           TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
                                   c->d_leaf_off, sm));
         }
+        tn::GemmArgs ga = sp.gemm;
+        ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
         Timer tm(c, 0, sp.tcc, sp.tmc);
-        TN_CUDA(tn::launch_gemm(sp.gemm, ps, c->num_sms, sm));
+        TN_CUDA(tn::launch_gemm(ga, ps, c->num_sms, sm));
       }
     }
   }
@@ -846,6 +850,8 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   c->device = device;
   c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   c->num_sms = prop.multiProcessorCount;
+  c->kchunk3 = env_int("TN_KCHUNK3", 1);
+  c->kchunk1 = env_int("TN_KCHUNK1", 0);
   *out = c;
   return TN_OK;
 }
@@ -1206,6 +1212,7 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     g.tiles_m = (int32_t)((m + 127) / 128);
     g.tiles_n = (int32_t)((n + 127) / 128);
     g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * J;
+    g.kchunk = passes == 3 ? c->kchunk3 : c->kchunk1;
     TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));
     cudaError_t e = cudaStreamSynchronize(sm);
     cudaFree(dp);

@@ -56,6 +56,8 @@ struct GemmArgs {
   double2* acc;                   // nullable: fused fp64 slice-accumulate
   int32_t tiles_m, tiles_n;
   int64_t n_tiles;
+  int32_t kchunk;                 // k-blocks per TMEM chunk promoted to the fp32 RN
+                                  // register sum (0 = whole K in TMEM); see DESIGN.md
 };
 
 // ---------------------------------------------------------------- slice select

@@ -88,6 +88,40 @@ def c2(n_slices: int = 64) -> Workload:
                     dict(meta, grid="5x6", cycles=14, open_qubits=10, n_slices=n_slices))
 
 
+def c4_base(boundary: str = "single", cycles: int = 18):
+    """Sycamore-53 m=18 circuit + boundary (no path): single amplitude, a 2^10
+    correlated subspace, or 2^k uniform samples ("sparse<k>")."""
+    circ = random_circuit(sycamore53_layout(), cycles, seed=1004)
+    net = circuit_to_network(circ)
+    if boundary == "single":
+        samples = single_amplitude(53, seed=2004)
+    elif boundary == "subspace":
+        samples = subspace_samples(53, list(range(43, 53)), seed=2004)
+    elif boundary.startswith("sparse"):
+        samples = uniform_samples(53, 1 << int(boundary[6:]), seed=2004)
+    else:
+        raise ValueError(boundary)
+    return Workload(f"c4_m{cycles}_{boundary}", circ, net, samples, [], [],
+                    {"layout": "sycamore53", "cycles": cycles, "boundary": boundary})
+
+
+def c4(boundary: str = "single", peak: int = 30) -> Workload:
+    """C4: Sycamore-53 m=18 with a cached SA + dynamic-slicing order file
+    (tools/make_orders.py); the bench times a subset of its slices (L542)."""
+    w = c4_base(boundary)
+    fn = _order_file(f"c4_{boundary}_p{peak}")
+    if not os.path.exists(fn):
+        raise FileNotFoundError(f"{fn} missing: run tools/make_orders.py c4 --peak {peak} "
+                                f"--boundary {boundary}")
+    with open(fn) as f:
+        d = json.load(f)
+    w.path = [tuple(p) for p in d["path"]]
+    w.sliced = list(d["sliced"])
+    w.meta.update(d.get("meta", {}))
+    w.name = f"c4_sycamore53_m18_{boundary}_p{peak}"
+    return w
+
+
 def small(grid=(3, 3), cycles=6, mode="sparse", n_samples=16, n_slices=4, seed=0,
           simplify=True) -> Workload:
     """Small seeded case for parity tests (oracle finishes in well under a second)."""
