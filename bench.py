@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
     ap.add_argument("--boundary", default="single")
-    ap.add_argument("--peak", type=int, default=30)
+    ap.add_argument("--peak", type=int, default=32)
     ap.add_argument("--precision", default="extended", choices=["extended", "mixed"])
     ap.add_argument("--topk", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -252,7 +252,7 @@ def run_ours(args):
                     "launches": g["launches"]}
 
     e2e = None
-    if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
+    if not args.no_e2e:
         ranks_, labels_, dims_, data_, opens_ = w.net.flat()
         host = np.ascontiguousarray(data_)
         n_e2e = max(1, min(args.steps, 3))

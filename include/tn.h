@@ -140,6 +140,8 @@ typedef struct {
   double bytes_per_slice;    /* Σ_steps T_mc (Eq. 5, 8 B per complex element)            */
   double peak_elements;      /* largest intermediate (elements)                          */
   int64_t device_bytes;      /* device memory held by the plan                           */
+  int64_t arena_bytes;       /* liveness-planned intermediate arena                      */
+  int64_t scratch_bytes;     /* fp16 operand-plane scratch of the largest tensor-core step */
 } tn_info;
 TN_API tn_status tn_get_info(tn_ctx* ctx, tn_info* info);
 

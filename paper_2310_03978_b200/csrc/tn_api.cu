@@ -1060,6 +1060,8 @@ tn_status tn_get_info(tn_ctx* c, tn_info* info) {
   info->bytes_per_slice = c->bytes_per_slice;
   info->peak_elements = c->peak;
   info->device_bytes = c->device_bytes;
+  info->arena_bytes = c->arena_elems * (int64_t)sizeof(float2);
+  info->scratch_bytes = c->scratch_bytes;
   return TN_OK;
 }
 

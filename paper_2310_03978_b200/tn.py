@@ -41,7 +41,8 @@ class Info(C.Structure):
     _fields_ = [("n_slices", C.c_int64), ("n_out", C.c_int64), ("n_steps", C.c_int32),
                 ("n_tc_steps", C.c_int32), ("flops_per_slice", C.c_double),
                 ("tc_flops_per_slice", C.c_double), ("bytes_per_slice", C.c_double),
-                ("peak_elements", C.c_double), ("device_bytes", C.c_int64)]
+                ("peak_elements", C.c_double), ("device_bytes", C.c_int64),
+                ("arena_bytes", C.c_int64), ("scratch_bytes", C.c_int64)]
 
 
 class KernelStats(C.Structure):
