@@ -120,15 +120,16 @@ def oracle_sample(w, target_flops, time_cap_s=60.0):
     pc = path_cost(w.net, w.samples, w.path, w.sliced)
     extra = []
     fine = list(w.sliced)
-    if pc.flops_per_slice > target_flops:
-        mult = 1
-        while pc.flops_per_slice / mult > target_flops:
-            mult *= 2
-        fine, pcf = slice_greedy(w.net, w.samples, w.path, n_slices=pc.n_slices * mult)
-        # keep the workload's own sliced bonds first so sub-slice 0 lies inside slice 0
-        extra = [x for x in fine if x not in w.sliced]
-        fine = list(w.sliced) + extra
-    pcs = path_cost(w.net, w.samples, w.path, fine)
+    pcs = pc
+    while pcs.flops_per_slice > target_flops and len(fine) < len(w.sliced) + 40:
+        # refine slice 0 by one more bond at a time (the workload's own sliced bonds
+        # stay first, so sub-slice 0 lies inside slice 0)
+        try:
+            fine, pcs = slice_greedy(w.net, w.samples, w.path, n_slices=pcs.n_slices * 2,
+                                     initial=fine, candidates_top=12)
+        except RuntimeError:
+            break
+        extra = fine[len(w.sliced):]
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     t0 = time.perf_counter()
     oracle.contract_slice(w.net, w.path, fine, 0, w.samples)

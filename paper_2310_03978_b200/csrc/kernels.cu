@@ -85,33 +85,105 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepDesc* __restrict__ 
   const float scale = ldexpf(1.0f, s);
   if (blockIdx.x == 0 && threadIdx.x == 0) *d.scale_out = s;
   const int64_t plane = d.plane_elems;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = idx % d.Kpad;
-    const int64_t rest = idx / d.Kpad;
-    const int64_t r = rest % d.R;
-    const int64_t g = rest / d.R;
-    float2 v = make_float2(0.f, 0.f);
-    if (k < d.K) {
-      int64_t off = g * d.g_stride;
-      int64_t t = r;
-      for (int i = d.nr - 1; i >= 0; --i) { off += (t % d.r_ext[i]) * d.r_s[i]; t /= d.r_ext[i]; }
-      t = k;
-      for (int i = d.nk - 1; i >= 0; --i) { off += (t % d.k_ext[i]) * d.k_s[i]; t /= d.k_ext[i]; }
-      v = src[off];
+  // Tiled transpose: a tile is TR rows x TK k-values of one slab.  Row and column
+  // source offsets are decomposed once per tile into smem, so each element costs
+  // one add; the read phase walks whichever of (r, k) has the smaller source
+  // stride (coalesced), the write phase walks k (K-contiguous planes).
+  constexpr int TR = 32, TK = 64;
+  __shared__ int64_t roff[TR];
+  __shared__ int64_t koff[TK];
+  __shared__ float2 tile[TR][TK + 1];
+  const bool r_fast = d.read_r_fast != 0;
+  const int64_t rtiles = (d.R + TR - 1) / TR, ktiles = (d.Kpad + TK - 1) / TK;
+  const int64_t ntiles = d.G * rtiles * ktiles;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t kt = t % ktiles;
+    const int64_t rt = (t / ktiles) % rtiles;
+    const int64_t g = t / (ktiles * rtiles);
+    const int64_t r0 = rt * TR, k0 = kt * TK;
+    __syncthreads();   // previous tile fully consumed
+    if (threadIdx.x < TR) {
+      int64_t r = r0 + threadIdx.x, off = -1;
+      if (r < d.R) {
+        off = g * d.g_stride;
+        for (int i = d.nr - 1; i >= 0; --i) { off += (r % d.r_ext[i]) * d.r_s[i]; r /= d.r_ext[i]; }
+      }
+      roff[threadIdx.x] = off;
+    } else if (threadIdx.x < TR + TK) {
+      int64_t k = k0 + threadIdx.x - TR, off = -1;
+      if (k < d.K) {
+        off = 0;
+        for (int i = d.nk - 1; i >= 0; --i) { off += (k % d.k_ext[i]) * d.k_s[i]; k /= d.k_ext[i]; }
+      }
+      koff[threadIdx.x - TR] = off;
     }
-    const float xr = v.x * scale, xi = v.y * scale;
-    const __half hr = __float2half_rn(xr), hi = __float2half_rn(xi);
-    d.dst[idx] = hr;
-    d.dst[plane + idx] = hi;
-    if (PLANES == 4) {   // residuals, RN (Eq. 8: small = rn(x - big))
-      d.dst[2 * plane + idx] = __float2half_rn(xr - __half2float(hr));
-      d.dst[3 * plane + idx] = __float2half_rn(xi - __half2float(hi));
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < TR * TK / 256; ++i) {
+      const int e = threadIdx.x + i * 256;
+      const int r = r_fast ? (e % TR) : (e / TK);
+      const int k = r_fast ? (e / TR) : (e % TK);
+      const int64_t ro = roff[r], ko = koff[k];
+      tile[r][k] = (ro >= 0 && ko >= 0) ? src[ro + ko] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < TR * TK / 512; ++i) {
+      const int e = threadIdx.x + i * 256;          // pairs of k
+      const int r = e / (TK / 2);
+      const int k = (e % (TK / 2)) * 2;
+      if (r0 + r >= d.R || k0 + k >= d.Kpad) continue;
+      const float2 v0 = tile[r][k], v1 = tile[r][k + 1];
+      const float xr0 = v0.x * scale, xi0 = v0.y * scale, xr1 = v1.x * scale, xi1 = v1.y * scale;
+      const __half2 hr = __floats2half2_rn(xr0, xr1), hi = __floats2half2_rn(xi0, xi1);
+      const int64_t idx = (g * d.R + r0 + r) * d.Kpad + k0 + k;   // Kpad even: half2-aligned
+      reinterpret_cast<__half2*>(d.dst + idx)[0] = hr;
+      reinterpret_cast<__half2*>(d.dst + plane + idx)[0] = hi;
+      if (PLANES == 4) {   // residuals, RN (Eq. 8: small = rn(x - big))
+        const float2 fr = __half22float2(hr), fi = __half22float2(hi);
+        reinterpret_cast<__half2*>(d.dst + 2 * plane + idx)[0] =
+            __floats2half2_rn(xr0 - fr.x, xr1 - fr.y);
+        reinterpret_cast<__half2*>(d.dst + 3 * plane + idx)[0] =
+            __floats2half2_rn(xi0 - fi.x, xi1 - fi.y);
+      }
     }
   }
 }
 
-// ---------------------------------------------------------------- SIMT einsum
+// Row-major digit decomposition of t over (ext[0..n-1]) -> Σ digit * stride.
+// Circuit networks have power-of-two extents: those dims use shift/mask.
+__device__ __forceinline__ int64_t decompose(int64_t t, int n, const int64_t* ext,
+                                             const int64_t* stride) {
+  int64_t off = 0;
+  for (int i = n - 1; i >= 0; --i) {
+    const int64_t e = ext[i];
+    if ((e & (e - 1)) == 0) {
+      off += (t & (e - 1)) * stride[i];
+      t >>= (__ffsll(e) - 1);
+    } else {
+      off += (t % e) * stride[i];
+      t /= e;
+    }
+  }
+  return off;
+}
+
+__device__ __forceinline__ void store_out(const EinsumDesc& d, int64_t idx, double cr, double ci,
+                                          float& amax) {
+  if (d.acc) {
+    double2 o = d.acc[idx];
+    o.x += cr;
+    o.y += ci;
+    d.acc[idx] = o;
+  } else {
+    d.C[idx] = make_float2((float)cr, (float)ci);
+  }
+  amax = fmaxf(amax, fmaxf(fabsf((float)cr), fabsf((float)ci)));
+}
+
+// ---------------------------------------------------------------- SIMT einsum, general
+// One thread per output C[j][m][n]; fp64 accumulation (a long fp32 RN chain would
+// cost ~2^-24·sqrt(K/2) relative).
 __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restrict__ gd,
                                                      const int64_t* __restrict__ leaf_off,
                                                      int64_t total) {
@@ -131,22 +203,12 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
     const int64_t t1 = idx / d.N;
     const int64_t m = t1 % d.M;
     const int64_t j = t1 / d.M;
-    int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs;
-    int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs;
-    int64_t t = m;
-    for (int i = d.nm - 1; i >= 0; --i) { ao += (t % d.m_ext[i]) * d.m_sa[i]; t /= d.m_ext[i]; }
-    t = n;
-    for (int i = d.nn - 1; i >= 0; --i) { bo += (t % d.n_ext[i]) * d.n_sb[i]; t /= d.n_ext[i]; }
-    // fp64 accumulation: a long fp32 RN chain would cost ~2^-24·sqrt(K/2) relative
+    const int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs + decompose(m, d.nm, d.m_ext, d.m_sa);
+    const int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs + decompose(n, d.nn, d.n_ext, d.n_sb);
     double cr = 0.0, ci = 0.0;
     for (int64_t ko = 0; ko < kouter; ++ko) {
-      int64_t ak = ao, bk = bo, u = ko;
-      for (int i = nk - 2; i >= 0; --i) {
-        const int64_t dg = u % d.k_ext[i];
-        u /= d.k_ext[i];
-        ak += dg * d.k_sa[i];
-        bk += dg * d.k_sb[i];
-      }
+      const int64_t ak = ao + decompose(ko, nk - 1, d.k_ext, d.k_sa);
+      const int64_t bk = bo + decompose(ko, nk - 1, d.k_ext, d.k_sb);
       for (int64_t ki = 0; ki < klast; ++ki) {
         const float2 a = A[ak + ki * ka_last];
         const float2 b = B[bk + ki * kb_last];
@@ -156,16 +218,119 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
         ci = fma((double)a.y, (double)b.x, ci);
       }
     }
-    if (d.acc) {
-      double2 o = d.acc[idx];
-      o.x += cr;
-      o.y += ci;
-      d.acc[idx] = o;
-    } else {
-      d.C[idx] = make_float2((float)cr, (float)ci);
-    }
-    amax = fmaxf(amax, fmaxf(fabsf((float)cr), fabsf((float)ci)));
+    store_out(d, idx, cr, ci, amax);
   }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+// ---------------------------------------------------------------- SIMT einsum, skinny
+// C[o][n][v] = Σ_k A[o, v, k] B[n, k] for a small B (N*K <= 8192 complex, staged
+// in smem once per block) and a big A streamed exactly once: lanes walk A's
+// smallest-stride free dim v (coalesced reads), the output keeps v innermost
+// (coalesced writes).  These are the HBM-bound "absorb a gate into the stem"
+// steps (stage 1 dominates).  fp32 accumulation (K <= 64 here).
+template <int NMAX>
+__global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __restrict__ gd,
+                                                            const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int K = (int)d.K, N = (int)d.N;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][N]
+  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * N);
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int k = e / N, n = e % N;
+    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
+  __syncthreads();
+  const int64_t V = d.V;
+  const int64_t vstride = d.m_sa[d.nm - 1];
+  const int64_t Mo = d.M / V;
+  float amax = 0.f;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < d.M;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t vi = m % V, o = m / V;
+    const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
+    float accr[NMAX], acci[NMAX];
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) { accr[n] = 0.f; acci[n] = 0.f; }
+    for (int k = 0; k < K; ++k) {
+      const float2 a = a_row[koff[k]];
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n < N) {
+          const float2 b = Bs[k * N + n];
+          accr[n] = fmaf(a.x, b.x, accr[n]);
+          accr[n] = fmaf(-a.y, b.y, accr[n]);
+          acci[n] = fmaf(a.x, b.y, acci[n]);
+          acci[n] = fmaf(a.y, b.x, acci[n]);
+        }
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n)
+      if (n < N) store_out(d, (o * N + n) * V + vi, accr[n], acci[n], amax);
+  }
+  (void)Mo;
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+// ---------------------------------------------------------------- SIMT einsum, split-K dot
+// Few outputs, long K (e.g. the last step of a closed network, a 2^30-long dot):
+// block b takes output p = b / nchunk and a kchunk range of k; fp64 block
+// reduction, fp64 atomicAdd into d.partial (zeroed before the launch).
+__global__ void __launch_bounds__(256) einsum_dot_kernel(const EinsumDesc* __restrict__ gd,
+                                                         const int64_t* __restrict__ leaf_off,
+                                                         int64_t nchunk) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  __shared__ double red[2][8];
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  const int64_t P = d.J * d.M * d.N;
+  for (int64_t blk = blockIdx.x; blk < P * nchunk; blk += gridDim.x) {
+    const int64_t p = blk / nchunk, c = blk % nchunk;
+    const int64_t n = p % d.N, t1 = p / d.N, m = t1 % d.M, j = t1 / d.M;
+    const int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs + decompose(m, d.nm, d.m_ext, d.m_sa);
+    const int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs + decompose(n, d.nn, d.n_ext, d.n_sb);
+    const int64_t k0 = c * d.kchunk, k1 = min(d.K, k0 + d.kchunk);
+    double cr = 0.0, ci = 0.0;
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      const float2 a = A[ao + decompose(k, d.nk, d.k_ext, d.k_sa)];
+      const float2 b = B[bo + decompose(k, d.nk, d.k_ext, d.k_sb)];
+      cr = fma((double)a.x, (double)b.x, cr);
+      cr = fma(-(double)a.y, (double)b.y, cr);
+      ci = fma((double)a.x, (double)b.y, ci);
+      ci = fma((double)a.y, (double)b.x, ci);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      cr += __shfl_xor_sync(0xffffffffu, cr, o);
+      ci += __shfl_xor_sync(0xffffffffu, ci, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { red[0][w] = cr; red[1][w] = ci; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sr = 0.0, si = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { sr += red[0][i]; si += red[1][i]; }
+      atomicAdd(&d.partial[2 * p], sr);
+      atomicAdd(&d.partial[2 * p + 1], si);
+    }
+  }
+}
+
+__global__ void einsum_dot_finalize(const EinsumDesc* __restrict__ gd) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  const int64_t P = d.J * d.M * d.N;
+  float amax = 0.f;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x)
+    store_out(d, p, d.partial[2 * p], d.partial[2 * p + 1], amax);
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
@@ -201,9 +366,31 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_einsum(const EinsumDesc* d_desc, int64_t total, const int64_t* leaf_off,
+cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off,
                           cudaStream_t s) {
   const int th = 256;
+  if (h.mode == 1) {
+    const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
+    const int g = grid_for(h.M, th);
+    if (h.N <= 4) einsum_skinny_kernel<4><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else if (h.N <= 8) einsum_skinny_kernel<8><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else if (h.N <= 16) einsum_skinny_kernel<16><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else if (h.N <= 32) einsum_skinny_kernel<32><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else einsum_skinny_kernel<64><<<g, th, smem, s>>>(d_desc, leaf_off);
+    return cudaGetLastError();
+  }
+  if (h.mode == 2) {
+    const int64_t P = h.J * h.M * h.N;
+    const int64_t nchunk = (h.K + h.kchunk - 1) / h.kchunk;
+    cudaError_t e = cudaMemsetAsync(h.partial, 0, sizeof(double) * 2 * P, s);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = P * nchunk;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    einsum_dot_kernel<<<(unsigned)blocks, th, 0, s>>>(d_desc, leaf_off, nchunk);
+    einsum_dot_finalize<<<grid_for(P, th), th, 0, s>>>(d_desc);
+    return cudaGetLastError();
+  }
+  const int64_t total = h.J * h.M * h.N;
   einsum_kernel<<<grid_for(total, th), th, 0, s>>>(d_desc, leaf_off, total);
   return cudaGetLastError();
 }

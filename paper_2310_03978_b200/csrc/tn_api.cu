@@ -73,6 +73,10 @@ struct StepPlan {
   int64_t prep_total[2] = {0, 0};
   int64_t R[2] = {0, 0}, Kpad = 0, G[2] = {1, 1};
   int in_slot[2] = {0, 0};
+  int mode = 0;                 // SIMT mode: 0 general, 1 skinny, 2 split-K dot
+  bool x_is_b = false;          // skinny: the big (streamed) operand is B
+  int64_t vlabel = 0;           // skinny: label of the lane (vector) dim
+  tn::EinsumDesc hdesc;         // host copy of the SIMT descriptor (launch parameters)
 };
 
 struct KStats {
@@ -145,6 +149,7 @@ struct tn_ctx {
   tn::EinsumDesc* d_einsum = nullptr;
   tn::PrepDesc* d_prep = nullptr;
   float2* d_one = nullptr;
+  double* d_partial = nullptr;     // split-K dot partial sums
   int64_t device_bytes = 0;
   // profiling
   bool profiling = false;
@@ -181,7 +186,7 @@ void free_dev(tn_ctx* c) {
   if (c->host_only) { c->planned = false; return; }
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
-                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one};
+                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_counter) cudaFreeHost(c->h_counter);
@@ -189,6 +194,7 @@ void free_dev(tn_ctx* c) {
   c->d_absmax = nullptr; c->d_scales = nullptr; c->d_leaf_off = nullptr; c->d_counter = nullptr;
   c->d_out_pos = nullptr; c->d_slice_desc = nullptr; c->d_terms_i = nullptr; c->d_terms_s = nullptr;
   c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr; c->h_counter = nullptr;
+  c->d_partial = nullptr;
   c->planned = false;
 }
 
@@ -286,6 +292,9 @@ tn_status build_plan(tn_ctx* c) {
   const int tc_small = env_int("TN_TC_MIN_SMALL", 16);
   const int tc_k = env_int("TN_TC_MIN_K", 16);
   const int disable_tc = env_int("TN_DISABLE_TC", 0);
+  const int skinny_big = env_int("TN_SKINNY_MIN_BIG", 1024);
+  const int dot_min_k = env_int("TN_DOT_MIN_K", 4096);
+  const int dot_max_out = env_int("TN_DOT_MAX_OUT", 4096);
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
 
@@ -320,6 +329,7 @@ tn_status build_plan(tn_ctx* c) {
   c->flops_per_slice = c->tc_flops = c->bytes_per_slice = c->peak = 0;
   for (auto& kv : live) c->peak = std::max(c->peak, (double)kv.second.size());
   int n_einsum = 0, n_prep = 0;
+  int64_t partial_elems = 0;
 
   for (int s = 0; s < n_steps; ++s) {
     StepPlan sp;
@@ -392,12 +402,44 @@ tn_status build_plan(tn_ctx* c) {
     sp.swap = sp.tc && sp.n > sp.m;   // tensor-core M side = larger free extent
 
     // output layout: [J][P dims][Q dims], P = A side unless swapped
+    // SIMT mode (see kernels.cu): 2 = split-K dot, 1 = skinny (one small operand)
+    if (!sp.tc) {
+      const int64_t outs = sp.J * sp.m * sp.n;
+      auto skinny = [&](int64_t big, int64_t small) {
+        return big >= skinny_big && small <= 64 && small * sp.k <= 8192 && sp.k <= 256;
+      };
+      const bool one_batch = !sp.merge || sp.J == 1;   // J = 1 merges fold their slabs
+      if (outs <= dot_max_out && sp.k >= dot_min_k) {
+        sp.mode = 2;
+        partial_elems = std::max(partial_elems, 2 * outs);
+      } else if (one_batch && skinny(sp.m, sp.n)) {
+        sp.mode = 1;
+        sp.x_is_b = false;
+      } else if (one_batch && skinny(sp.n, sp.m)) {
+        sp.mode = 1;
+        sp.x_is_b = true;
+      }
+    }
     std::vector<VDim> od;
-    if (sp.merge) od.push_back({GROUP, sp.J, 0});
-    const auto& P = sp.swap ? FB : FA;
-    const auto& Q = sp.swap ? FA : FB;
-    for (auto& d : P) od.push_back({d.label, d.ext, 0});
-    for (auto& d : Q) od.push_back({d.label, d.ext, 0});
+    if (sp.mode == 1) {
+      // output [X outer dims][Y dims][v], v = the big operand's smallest-stride dim
+      const auto& X = sp.x_is_b ? FB : FA;
+      const auto& Y = sp.x_is_b ? FA : FB;
+      int vi = -1;
+      for (int p = 0; p < (int)X.size(); ++p)
+        if (X[p].ext > 1 && (vi < 0 || X[p].stride < X[vi].stride)) vi = p;
+      sp.vlabel = X[vi].label;
+      for (int p = 0; p < (int)X.size(); ++p)
+        if (p != vi) od.push_back({X[p].label, X[p].ext, 0});
+      for (auto& d : Y) od.push_back({d.label, d.ext, 0});
+      od.push_back({X[vi].label, X[vi].ext, 0});
+    } else {
+      if (sp.merge) od.push_back({GROUP, sp.J, 0});
+      const auto& P = sp.swap ? FB : FA;
+      const auto& Q = sp.swap ? FA : FB;
+      for (auto& d : P) od.push_back({d.label, d.ext, 0});
+      for (auto& d : Q) od.push_back({d.label, d.ext, 0});
+    }
     contiguous_strides(od);
     out.dims = od;
     out.buf = 1;
@@ -482,6 +524,7 @@ tn_status build_plan(tn_ctx* c) {
   if ((st = dev_alloc(c, &c->d_einsum, (size_t)std::max(n_einsum, 1)))) return st;
   if ((st = dev_alloc(c, &c->d_prep, (size_t)std::max(n_prep, 1)))) return st;
   if ((st = dev_alloc(c, &c->d_one, 1))) return st;
+  if ((st = dev_alloc(c, &c->d_partial, (size_t)std::max<int64_t>(partial_elems, 2)))) return st;
   TN_CUDA(cudaMallocHost(&c->h_counter, sizeof(int64_t)));
   cudaStream_t sm = c->stream;
   if (!tables.empty())
@@ -563,6 +606,8 @@ tn_status build_plan(tn_ctx* c) {
       if (sp.merge && d.label == GROUP) { gB = d; continue; }
       FB.push_back(d);
     }
+    const std::vector<VDim> FA0 = FA, FB0 = FB;
+    const std::vector<KDim> K0 = K;
     coalesce1(FA);
     coalesce1(FB);
     coalesce2(K);
@@ -570,7 +615,53 @@ tn_status build_plan(tn_ctx* c) {
       return fail(TN_ERR_INTERNAL, "step " + std::to_string(s) + ": too many non-coalescable dims");
     unsigned* absmax_out = sp.final_step ? nullptr : c->d_absmax + (n_leaves + s);
     float2* Cptr = sp.final_step ? nullptr : c->d_arena + sp.out_off;
-    if (!sp.tc) {
+    if (!sp.tc && sp.mode == 1) {
+      // skinny: X = big operand (streamed), Y = small operand (smem); out [Xo][Y][v]
+      const View& XV = sp.x_is_b ? B : A;
+      const View& YV = sp.x_is_b ? A : B;
+      const auto& X0 = sp.x_is_b ? FB0 : FA0;
+      std::vector<VDim> Xo, Ys = sp.x_is_b ? FA0 : FB0;
+      VDim v{0, 1, 0};
+      for (auto& d : X0) {
+        if (d.label == sp.vlabel) v = d;
+        else Xo.push_back(d);
+      }
+      coalesce1(Xo);
+      coalesce1(Ys);
+      std::vector<KDim> Kx = K0;
+      if (sp.x_is_b) for (auto& x : Kx) std::swap(x.sa, x.sb);
+      coalesce2(Kx);
+      if ((int)Xo.size() + 1 > TN_MAXD || (int)Ys.size() > TN_MAXD || (int)Kx.size() > TN_MAXD)
+        return fail(TN_ERR_INTERNAL, "step " + std::to_string(s) + ": too many dims (skinny)");
+      tn::EinsumDesc& e = eds[sp.einsum_idx];
+      memset(&e, 0, sizeof(e));
+      e.mode = 1;
+      e.A = base_of(XV); e.B = base_of(YV); e.C = Cptr;
+      e.a_off = XV.off; e.b_off = YV.off;
+      if (sp.merge) {   // J == 1: fold the single slab of each side into the offsets
+        const int64_t sa = (int64_t)sp.ia[0] * gA.stride, sb = (int64_t)sp.ib[0] * gB.stride;
+        e.a_off += sp.x_is_b ? sb : sa;
+        e.b_off += sp.x_is_b ? sa : sb;
+      }
+      e.a_leaf = XV.buf == 0 ? XV.leaf : -1;
+      e.b_leaf = YV.buf == 0 ? YV.leaf : -1;
+      e.J = 1;
+      e.M = sp.x_is_b ? sp.n : sp.m;
+      e.N = sp.x_is_b ? sp.m : sp.n;
+      e.K = sp.k;
+      e.V = v.ext;
+      e.nm = (int)Xo.size() + 1;
+      for (int p = 0; p < (int)Xo.size(); ++p) { e.m_ext[p] = Xo[p].ext; e.m_sa[p] = Xo[p].stride; }
+      e.m_ext[e.nm - 1] = v.ext;
+      e.m_sa[e.nm - 1] = v.stride;
+      e.nn = (int)Ys.size();
+      for (int p = 0; p < e.nn; ++p) { e.n_ext[p] = Ys[p].ext; e.n_sb[p] = Ys[p].stride; }
+      e.nk = (int)Kx.size();
+      for (int p = 0; p < e.nk; ++p) { e.k_ext[p] = Kx[p].ext; e.k_sa[p] = Kx[p].sa; e.k_sb[p] = Kx[p].sb; }
+      e.absmax_out = absmax_out;
+      e.acc = sp.final_step ? c->d_acc : nullptr;
+      sp.hdesc = e;
+    } else if (!sp.tc) {
       tn::EinsumDesc& e = eds[sp.einsum_idx];
       memset(&e, 0, sizeof(e));
       e.A = base_of(A); e.B = base_of(B); e.C = Cptr;
@@ -588,6 +679,12 @@ tn_status build_plan(tn_ctx* c) {
       for (int p = 0; p < e.nk; ++p) { e.k_ext[p] = K[p].ext; e.k_sa[p] = K[p].sa; e.k_sb[p] = K[p].sb; }
       e.absmax_out = absmax_out;
       e.acc = sp.final_step ? c->d_acc : nullptr;
+      if (sp.mode == 2) {
+        e.mode = 2;
+        e.partial = c->d_partial;
+        e.kchunk = 1 << 16;
+      }
+      sp.hdesc = e;
     } else {
       // P operand = A side unless swapped; both share the canonical K order
       for (int side = 0; side < 2; ++side) {
@@ -608,9 +705,14 @@ tn_status build_plan(tn_ctx* c) {
         for (int d = 0; d < p.nr; ++d) { p.r_ext[d] = F[d].ext; p.r_s[d] = F[d].stride; }
         std::vector<VDim> kd;
         for (auto& x : K) kd.push_back({0, x.ext, fromA ? x.sa : x.sb});
-        // (K already coalesced jointly; keep as is)
+        coalesce1(kd);   // per-operand merge keeps the shared row-major k order
         p.nk = (int)kd.size();
         for (int d = 0; d < p.nk; ++d) { p.k_ext[d] = kd[d].ext; p.k_s[d] = kd[d].stride; }
+        {
+          const int64_t rs = p.nr ? p.r_s[p.nr - 1] : INT64_MAX;
+          const int64_t ks = p.nk ? p.k_s[p.nk - 1] : INT64_MAX;
+          p.read_r_fast = rs < ks ? 1 : 0;
+        }
         int64_t off0 = 0;
         int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
         if (side == 1) off0 = bytes0;
@@ -699,7 +801,7 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
       StepPlan& sp = c->steps[s];
       if (!sp.tc) {
         Timer tm(c, 2, sp.tcc, sp.tmc);
-        TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.J * sp.m * sp.n, c->d_leaf_off, sm));
+        TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm));
       } else {
         const int ps = passes[s];
         const int planes = ps == 3 ? 4 : 2;
@@ -1077,9 +1179,9 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     char b[512];
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
-             "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"ia\":",
+             "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
-             sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false");
+             sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode);
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";
@@ -1169,7 +1271,7 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     tn::EinsumDesc* d = nullptr;
     TN_CUDA(cudaMalloc(&d, sizeof(e)));
     TN_CUDA(cudaMemcpyAsync(d, &e, sizeof(e), cudaMemcpyHostToDevice, sm));
-    TN_CUDA(tn::launch_einsum(d, J * m * n, nullptr, sm));
+    TN_CUDA(tn::launch_einsum(d, e, nullptr, sm));
     TN_CUDA(cudaStreamSynchronize(sm));
     cudaFree(d);
   } else {
@@ -1191,6 +1293,7 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
       p[side].g_stride = R * k;
       p[side].nr = 1; p[side].r_ext[0] = R; p[side].r_s[0] = k;
       p[side].nk = 1; p[side].k_ext[0] = k; p[side].k_s[0] = 1;
+      p[side].read_r_fast = 0;
       p[side].dst = reinterpret_cast<__half*>(scr + (side ? b0 : 0));
       p[side].plane_elems = G * R * Kpad;
       p[side].absmax_in = am + side;

@@ -27,6 +27,13 @@ struct EinsumDesc {
   int64_t k_ext[TN_MAXD], k_sa[TN_MAXD], k_sb[TN_MAXD];
   unsigned* absmax_out;           // nullable: atomicMax of |re|,|im| bits
   double2* acc;                   // nullable: acc[idx] += C instead of storing C
+  // mode: 0 general (one thread per output), 1 skinny (B = small operand staged in
+  // smem, output layout [Mo][N][V] with V = A's smallest-stride free dim, which is
+  // m_ext/m_sa[nm-1] here), 2 split-K dot (few outputs, long K; fp64 partials)
+  int32_t mode, pad_;
+  int64_t V;                      // mode 1: extent of the vector (lane) dim
+  double* partial;                // mode 2: fp64 partial sums [2*J*M*N] (zeroed per launch)
+  int64_t kchunk;                 // mode 2: k elements per block
 };
 
 // ---------------------------------------------------------------- operand prep
@@ -39,6 +46,7 @@ struct PrepDesc {
   int32_t nr, nk;
   int64_t r_ext[TN_MAXD], r_s[TN_MAXD];
   int64_t k_ext[TN_MAXD], k_s[TN_MAXD];
+  int32_t read_r_fast, pad_;      // 1: source stride of rows < of k (read along r)
   __half* dst; int64_t plane_elems;
   const unsigned* absmax_in;      // absmax of the source tensor (float bits)
   int* scale_out;                 // receives the exponent s (x * 2^s is split)
@@ -76,8 +84,8 @@ struct SliceDesc {
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes,
                         const int64_t* leaf_off, cudaStream_t s);
-cudaError_t launch_einsum(const EinsumDesc* d_desc, int64_t total, const int64_t* leaf_off,
-                          cudaStream_t s);
+cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
+                          const int64_t* leaf_off, cudaStream_t s);
 cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
                               cudaStream_t s);
 cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);

@@ -118,18 +118,30 @@ def run_gpu(ctx, w, precision="extended", topk=10, slices=None):
     return out, info
 
 
+ROUTES = {
+    "simt": {"TN_DISABLE_TC": "1"},
+    "simt_modes": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_DOT_MIN_K": "2",
+                   "TN_DOT_MAX_OUT": "16"},
+    "tc": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2"},
+    "default": {},
+}
+
+
 @pytest.mark.parametrize("mode", ["sparse", "full", "single", "subspace"])
-@pytest.mark.parametrize("tc", [False, True])
-def test_contraction_vs_oracle(ctx, mode, tc, monkeypatch):
-    if tc:
-        monkeypatch.setenv("TN_TC_MIN_BIG", "8")
-        monkeypatch.setenv("TN_TC_MIN_SMALL", "2")
-        monkeypatch.setenv("TN_TC_MIN_K", "2")
+@pytest.mark.parametrize("route", list(ROUTES))
+def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
+    for k, v in ROUTES[route].items():
+        monkeypatch.setenv(k, v)
     w = configs.small(grid=(3, 4), cycles=8, mode=mode, n_samples=64, n_slices=8, seed=2)
     ref = oracle.contract(w.net, w.path, w.sliced, w.samples)
     out, info = run_gpu(ctx, w)
-    if tc:
+    if route == "tc":
         assert info["n_tc_steps"] > 0
+    if route == "simt_modes":
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        modes = {s["mode"] for s in c.plan_json()["steps"]}
+        assert {1, 2} <= modes, modes
     assert rel_l2(out, ref) <= EXT_TOL
     out_m, _ = run_gpu(ctx, w, precision="mixed", topk=10)
     assert rel_l2(out_m, ref) <= MIX_TOL

@@ -273,13 +273,14 @@ def bisection_path(net, samples=None, seed: int = 0, leaf_size: int = 12,
 # ----------------------------------------------------------------------------- slicing
 
 def slice_greedy(net, samples, path, n_slices: int | None = None,
-                 peak_log2: float | None = None, candidates_top: int = 4):
+                 peak_log2: float | None = None, candidates_top: int = 4, initial=()):
     """Greedily slice closed bonds (L292-295) until ``n_slices`` is reached and/or the
-    largest intermediate is <= 2**peak_log2.  Returns the ordered sliced-label list
-    (the last one is the fastest-varying digit of the slice index)."""
+    largest intermediate is <= 2**peak_log2, starting from the ``initial`` slice
+    list.  Returns the ordered sliced-label list (the last one is the
+    fastest-varying digit of the slice index)."""
     sm = SampleModel(net.n_qubits, samples)
     open_set = set(net.open_labels)
-    sliced = []
+    sliced = list(initial)
 
     def done(pc):
         ok = True
@@ -293,15 +294,20 @@ def slice_greedy(net, samples, path, n_slices: int | None = None,
     while not done(pc):
         # candidate labels: those of the largest intermediates
         st = _leaf_state(net, frozenset(sliced))
-        outs = []
+        outs, costly = [], []
         for i, j in path:
+            labs = st[i][0] | st[j][0]
             res, info = _step(st[i], st[j], net.dims, sm)
             st[i] = res
             del st[j]
             outs.append((info.out_log2, res[0]))
+            costly.append((info.flops, labs))
         outs.sort(key=lambda t: -t[0])
+        costly.sort(key=lambda t: -t[0])
         cands = set()
         for _, L in outs[:candidates_top]:
+            cands |= set(L)
+        for _, L in costly[:candidates_top]:     # bonds of the most expensive steps
             cands |= set(L)
         cands -= open_set
         cands -= set(sliced)
