@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
     ap.add_argument("--boundary", default="single")
     ap.add_argument("--peak", type=int, default=32)
+    ap.add_argument("--order-tag", default="a64", help="order file variant (tools/make_orders.py)")
     ap.add_argument("--precision", default="extended", choices=["extended", "mixed"])
     ap.add_argument("--topk", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -56,7 +57,7 @@ def load_workload(args):
     from tnworkloads import configs
     if args.workload == "c2":
         return configs.c2()
-    return configs.c4(args.boundary, args.peak)
+    return configs.c4(args.boundary, args.peak, args.order_tag)
 
 
 def measured_peaks():
@@ -120,16 +121,13 @@ def oracle_sample(w, target_flops, time_cap_s=60.0):
     pc = path_cost(w.net, w.samples, w.path, w.sliced)
     extra = []
     fine = list(w.sliced)
-    pcs = pc
-    while pcs.flops_per_slice > target_flops and len(fine) < len(w.sliced) + 40:
-        # refine slice 0 by one more bond at a time (the workload's own sliced bonds
-        # stay first, so sub-slice 0 lies inside slice 0)
-        try:
-            fine, pcs = slice_greedy(w.net, w.samples, w.path, n_slices=pcs.n_slices * 2,
-                                     initial=fine, candidates_top=12)
-        except RuntimeError:
-            break
+    if pc.flops_per_slice > target_flops:
+        # refine slice 0 with extra bonds (the workload's own sliced bonds stay first,
+        # so sub-slice 0 lies inside slice 0)
+        from tnworkloads.treesa import refine_slices
+        fine, _ = refine_slices(w.net, w.samples, w.path, w.sliced, target_flops, max_extra=48)
         extra = fine[len(w.sliced):]
+    pcs = path_cost(w.net, w.samples, w.path, fine)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     t0 = time.perf_counter()
     oracle.contract_slice(w.net, w.path, fine, 0, w.samples)

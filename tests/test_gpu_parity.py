@@ -186,6 +186,37 @@ def test_echo_exact(ctx, force_tc):
     assert np.abs(out[~is0]).max() < 1e-5
 
 
+def _refine(w, target_flops):
+    """Extra sliced bonds (appended after the workload's own) until a sub-slice
+    costs <= target_flops; sub-slice t*2^e .. (t+1)*2^e-1 tile coarse slice t."""
+    from tnworkloads.paths import path_cost
+    from tnworkloads.treesa import refine_slices
+    fine, _ = refine_slices(w.net, w.samples, w.path, w.sliced, target_flops, max_extra=48)
+    return fine, path_cost(w.net, w.samples, w.path, fine)
+
+
+@pytest.mark.timeout(900)
+def test_c4_bench_workload_sampled_subslice(ctx):
+    """The bench workload (Sycamore-53 m=18, C4 order file) at full width: one
+    sub-slice of slice 0 compared element-by-element with the oracle (the oracle
+    cannot afford a whole 3e14-flop slice), plus the slicing identity on GPU:
+    a coarse slice equals the sum of its sub-slices."""
+    w = configs.c4()
+    fine, pc = _refine(w, 4e11)
+    extra = len(fine) - len(w.sliced)
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(w.net, w.samples, w.path, fine)
+    c.contract(0, 1)
+    got = c.sum_slices_host()
+    info = c.info()
+    c.close()
+    ref = oracle.contract_slice(w.net, w.path, fine, 0, w.samples)
+    err = rel_l2(got, ref)
+    print(f"C4 sub-slice: extra bonds {extra}, T_cc {pc.flops_per_slice:.3g}, "
+          f"tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}")
+    assert err <= EXT_TOL
+
+
 def test_c2_sampled_slices_at_full_size(ctx):
     """C2 at full size (30 q, 2^10 amplitudes, the 64-slice plan the bench times):
     a GPU slice equals the sum of its GPU sub-slices (slicing identity, any size),

@@ -105,20 +105,21 @@ def c4_base(boundary: str = "single", cycles: int = 18):
                     {"layout": "sycamore53", "cycles": cycles, "boundary": boundary})
 
 
-def c4(boundary: str = "single", peak: int = 30) -> Workload:
+def c4(boundary: str = "single", peak: int = 32, tag: str = "a64") -> Workload:
     """C4: Sycamore-53 m=18 with a cached SA + dynamic-slicing order file
-    (tools/make_orders.py); the bench times a subset of its slices (L542)."""
+    (tools/make_orders.py; tag "a64" = Eq. 6 score with alpha = 64 flop/B); the
+    bench times a subset of its slices and extrapolates (L542)."""
     w = c4_base(boundary)
-    fn = _order_file(f"c4_{boundary}_p{peak}")
+    fn = _order_file(f"c4_{boundary}_p{peak}{tag}")
     if not os.path.exists(fn):
         raise FileNotFoundError(f"{fn} missing: run tools/make_orders.py c4 --peak {peak} "
-                                f"--boundary {boundary}")
+                                f"--boundary {boundary} --alpha ... --tag {tag}")
     with open(fn) as f:
         d = json.load(f)
     w.path = [tuple(p) for p in d["path"]]
     w.sliced = list(d["sliced"])
     w.meta.update(d.get("meta", {}))
-    w.name = f"c4_sycamore53_m18_{boundary}_p{peak}"
+    w.name = f"c4_sycamore53_m18_{boundary}_p{peak}{tag}"
     return w
 
 

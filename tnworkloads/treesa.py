@@ -70,24 +70,30 @@ class Tree:
             self._ucache[qmask] = v
         return v
 
+    alpha = 0.0     # Eq. 6 memory weight: flop-equivalents per byte of T_mc (8 B/element)
+
     def pair_cost(self, La, Qa, Lb, Qb, keep):
-        """(log2 flops, log2 out size) of contracting (La,Qa) with (Lb,Qb); keep = ~sliced."""
+        """(cost, log2 out size) of contracting (La,Qa) with (Lb,Qb); keep = ~sliced.
+        cost = T_cc + alpha * T_mc (the argument of the log in Eq. 6)."""
         La &= keep
         Lb &= keep
         K = La & Lb
         lk = K.bit_count()
         lm = (La & ~K).bit_count()
         ln = (Lb & ~K).bit_count()
+        ua, ub = self.log2U(Qa), self.log2U(Qb)
         if Qa and Qb:
             lj = self.log2U(Qa | Qb)
         else:
             lj = 0.0
-            if Qa:
-                lm += self.log2U(Qa)
-            if Qb:
-                ln += self.log2U(Qb)
+            lm += ua
+            ln += ub
         out = (La ^ Lb).bit_count() + self.log2U(Qa | Qb)
-        return lj + lm + ln + lk + 3.0, out
+        cost = 2.0 ** (lj + lm + ln + lk + 3.0)
+        if self.alpha:
+            cost += self.alpha * 8.0 * (2.0 ** (La.bit_count() + ua) + 2.0 ** (Lb.bit_count() + ub)
+                                        + 2.0 ** out)
+        return cost, out
 
     def node_cost(self, v, keep):
         a, b = self.left[v], self.right[v]
@@ -101,7 +107,7 @@ class Tree:
         peak = 0.0
         for v in self.internal():
             f, s = self.node_cost(v, keep)
-            tot += 2.0 ** f
+            tot += f
             peak = max(peak, s)
         return tot, peak
 
@@ -112,7 +118,7 @@ class Tree:
         tot = 0.0
         for v in nodes:
             f, _ = self.node_cost(v, keep)
-            flops[v] = 2.0 ** f
+            flops[v] = f
             tot += flops[v]
         for sw in range(sweeps):
             T = t0 * (t1 / t0) ** (sw / max(sweeps - 1, 1))
@@ -132,7 +138,7 @@ class Tree:
                     continue
                 Ly, Qy = self.L[Y1] ^ self.L[Z], self.Q[Y1] | self.Q[Z]
                 fx, _ = self.pair_cost(Ly, Qy, self.L[Y2], self.Q[Y2], keep)
-                new = 2.0 ** fy + 2.0 ** fx
+                new = fy + fx
                 old = flops[X] + flops[Y]
                 tot_new = tot - old + new
                 dE = math.log2(tot_new) - math.log2(tot)
@@ -144,8 +150,8 @@ class Tree:
                     self.left[X], self.right[X] = Y, Y2
                     self.parent[Y2] = X
                     self.L[Y], self.Q[Y] = Ly, Qy
-                    flops[Y] = 2.0 ** fy
-                    flops[X] = 2.0 ** fx
+                    flops[Y] = fy
+                    flops[X] = fx
                     tot = tot_new
         return tot
 
@@ -170,14 +176,45 @@ class Tree:
         return pairs
 
 
+def refine_slices(net, samples, path, sliced, target_flops: float, max_extra: int = 40):
+    """Keep ``path`` fixed and append bonds to ``sliced`` (greedy, min per-slice flops)
+    until one sub-slice costs <= target_flops.  Sub-slices of coarse slice t are
+    t*2^e .. (t+1)*2^e - 1 (the new bonds are the fastest digits).  Used to size
+    oracle-checkable samples of a large workload."""
+    tr = Tree(net, samples, path)
+    keep = (1 << len(tr.label_of)) - 1
+    for x in sliced:
+        keep &= ~(1 << tr.bit[x])
+    extra = []
+    tot, _ = tr.totals(keep)
+    while tot > target_flops and len(extra) < max_extra:
+        best = None
+        b = keep
+        while b:
+            low = b & -b
+            bit = low.bit_length() - 1
+            b ^= low
+            t2, _ = tr.totals(keep & ~(1 << bit))
+            if best is None or t2 < best[1]:
+                best = (bit, t2)
+        if best is None or best[1] >= tot:
+            break
+        keep &= ~(1 << best[0])
+        extra.append(tr.label_of[best[0]])
+        tot = best[1]
+    return list(sliced) + extra, tot
+
+
 def optimize(net, samples, path0, peak_log2: float, seed: int = 0, sweeps: int = 40,
              fine_sweeps: int = 6, t0: float = 0.3, t1: float = 0.01, max_slices: int = 64,
-             cand_top: int = 48, log=None):
+             cand_top: int = 48, log=None, alpha: float = 0.0):
     """SA on the unsliced tree, then dynamic slicing down to ``peak_log2`` with a
-    short low-temperature re-tune after every cut.  Returns (path, sliced labels,
-    per-slice flops, peak log2)."""
+    short low-temperature re-tune after every cut.  The score is Eq. 6's
+    T_cc + alpha*T_mc (alpha in flop per byte).  Returns (path, sliced labels,
+    per-slice cost, peak log2)."""
     rng = np.random.default_rng(seed)
     tr = Tree(net, samples, path0)
+    tr.alpha = alpha
     full = (1 << len(tr.label_of)) - 1
     tr.anneal(full, sweeps, t0, t1, None, rng)
     sliced_bits = []

@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--sweeps", type=int, default=60)
     ap.add_argument("--boundary", default="single")
+    ap.add_argument("--alpha", type=float, default=0.0,
+                    help="Eq. 6 memory weight (flop-equivalents per byte of T_mc)")
+    ap.add_argument("--tag", default="")
     args = ap.parse_args()
     w = configs.c4_base(boundary=args.boundary)
     best = None
@@ -30,18 +33,21 @@ def main():
         t = time.time()
         p0 = bisection_path(w.net, w.samples, seed=3004 + s, leaf_size=8, time_weight=0.3)
         path, sliced, tot, pk = optimize(w.net, w.samples, p0, args.peak, seed=3004 + s,
-                                         sweeps=args.sweeps)
+                                         sweeps=args.sweeps, alpha=args.alpha)
         pc = path_cost(w.net, w.samples, path, sliced)
+        score = tot * 2.0 ** len(sliced)
         print(f"seed {s}: per-slice {pc.flops_per_slice:.3g} peak 2^{pc.peak_log2:.1f} "
-              f"slices 2^{len(sliced)} total {pc.total_flops:.3g} ({time.time() - t:.0f}s)", flush=True)
-        if best is None or pc.total_flops < best[2].total_flops:
-            best = (path, sliced, pc, s)
-    path, sliced, pc, s = best
+              f"slices 2^{len(sliced)} total {pc.total_flops:.3g} score {score:.3g} "
+              f"({time.time() - t:.0f}s)", flush=True)
+        if best is None or score < best[4]:
+            best = (path, sliced, pc, s, score)
+    path, sliced, pc, s, score = best
     meta = {"method": "bisection(KL, time_weight 0.3) + tree SA + dynamic slicing",
+            "score": "Eq. 6 T_cc + alpha*T_mc", "alpha": args.alpha,
             "seed": 3004 + s, "peak_log2_target": args.peak, "sweeps": args.sweeps,
             "flops_per_slice": pc.flops_per_slice, "peak_log2": pc.peak_log2,
             "n_sliced": len(sliced), "boundary": args.boundary}
-    fn = configs._order_file(f"{args.name}_{args.boundary}_p{int(args.peak)}")
+    fn = configs._order_file(f"{args.name}_{args.boundary}_p{int(args.peak)}{args.tag}")
     os.makedirs(os.path.dirname(fn), exist_ok=True)
     with open(fn, "w") as f:
         json.dump({"path": [list(map(int, p)) for p in path], "sliced": [int(x) for x in sliced],
