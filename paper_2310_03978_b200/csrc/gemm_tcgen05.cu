@@ -140,6 +140,27 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Tile index -> (j, mt, nt).  Tiles of one batch are visited in groups of
+// `group_m` tile rows, column-major inside a group, so the ~148 tiles resident
+// at once share few A and B panels in L2.
+__device__ __forceinline__ void decode_tile(const GemmArgs& a, int64_t tile, int& j, int& mt, int& nt) {
+  const int64_t per_j = (int64_t)a.tiles_m * a.tiles_n;
+  j = (int)(tile / per_j);
+  const int rem = (int)(tile % per_j);
+  if (a.group_m > 1) {
+    const int gsz = a.group_m * a.tiles_n;
+    const int g = rem / gsz;
+    const int first = g * a.group_m;
+    const int gm = min(a.tiles_m - first, a.group_m);
+    const int r = rem % gsz;
+    mt = first + r % gm;
+    nt = r / gm;
+  } else {
+    mt = rem / a.tiles_n;
+    nt = rem % a.tiles_n;
+  }
+}
+
 template <int PASSES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<PASSES>;
@@ -157,7 +178,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
   const int kblocks = (args.K + BK - 1) / BK;
   const int kchunk = (args.kchunk > 0 && args.kchunk < kblocks) ? args.kchunk : kblocks;
   const int nchunks = (kblocks + kchunk - 1) / kchunk;
-  const int64_t per_j = (int64_t)args.tiles_m * args.tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -189,9 +209,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
-        const int j = (int)(tile / per_j);
-        const int rem = (int)(tile % per_j);
-        const int mt = rem / args.tiles_n, nt = rem % args.tiles_n;
+        int j, mt, nt;
+        decode_tile(args, tile, j, mt, nt);
         const int sa = args.ia ? args.ia[j] : 0;
         const int sb = args.ib ? args.ib[j] : 0;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -231,34 +250,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint32_t st = smem_u32(smem + stage * C::STAGE_BYTES);
+          if (PASSES == 3) {
+            // Eq. 8, small terms first: every hi·lo / lo·hi MMA of the stage is
+            // issued while the chunk accumulator is still ~2^-11 of its final size,
+            // so the per-MMA RZ truncation only bites on the big·big MMAs.
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t koff = kk * 32;   // 16 fp16 = 32 B along K inside the swizzle row
-            const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
-            const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
-            const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
-            const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
-            const uint32_t acc0 = (kin | kk) != 0;
-            if (PASSES == 3) {
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t koff = kk * 32;   // 16 fp16 = 32 B along K inside the swizzle row
+              const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
+              const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
+              const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
+              const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
               const uint64_t arl = sdesc(st + 2 * PLANE_TILE + koff);
               const uint64_t ail = sdesc(st + 3 * PLANE_TILE + koff);
               const uint64_t brl = sdesc(st + (PLANES + 2) * PLANE_TILE + koff);
               const uint64_t bil = sdesc(st + (PLANES + 3) * PLANE_TILE + koff);
-              // real part: Ar·Br - Ai·Bi  (small terms first, Eq. 8)
+              const uint32_t acc0 = (kin | kk) != 0;
+              // real part: Ar·Br - Ai·Bi (cross terms)
               mma(d_re, ar, brl, IDESC, acc0);
               mma(d_re, arl, br, IDESC, 1);
               mma(d_re, ail, bi, IDESC_NEG, 1);
               mma(d_re, ai, bil, IDESC_NEG, 1);
-              mma(d_re, ar, br, IDESC, 1);
-              mma(d_re, ai, bi, IDESC_NEG, 1);
-              // imaginary part: Ar·Bi + Ai·Br
+              // imaginary part: Ar·Bi + Ai·Br (cross terms)
               mma(d_im, ar, bil, IDESC, acc0);
               mma(d_im, arl, bi, IDESC, 1);
               mma(d_im, ai, brl, IDESC, 1);
               mma(d_im, ail, br, IDESC, 1);
+            }
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t koff = kk * 32;
+              const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
+              const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
+              const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
+              const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
+              mma(d_re, ar, br, IDESC, 1);        // big·big last
+              mma(d_re, ai, bi, IDESC_NEG, 1);
               mma(d_im, ar, bi, IDESC, 1);
               mma(d_im, ai, br, IDESC, 1);
-            } else {
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t koff = kk * 32;
+              const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
+              const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
+              const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
+              const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
+              const uint32_t acc0 = (kin | kk) != 0;
               mma(d_re, ar, br, IDESC, acc0);
               mma(d_re, ai, bi, IDESC_NEG, 1);
               mma(d_im, ar, bi, IDESC, acc0);
@@ -290,9 +329,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
     int cb = 0;
     uint32_t cphase = 0;
     for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
-      const int j = (int)(tile / per_j);
-      const int rem = (int)(tile % per_j);
-      const int mt = rem / args.tiles_n, nt = rem % args.tiles_n;
+      int j, mt, nt;
+      decode_tile(args, tile, j, mt, nt);
       float sr[64], si[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) { sr[i] = 0.f; si[i] = 0.f; }

@@ -278,6 +278,54 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// ---------------------------------------------------------------- SIMT einsum, wide skinny
+// Same layout contract as einsum_skinny_kernel (out [Mo][N][V]) for outer-product-
+// like steps: K <= KMAX (the big operand's row lives in registers), N up to 4096
+// (small operand staged in smem), outputs streamed n by n with lanes along v.
+template <int KMAX>
+__global__ void __launch_bounds__(256) einsum_wide_kernel(const EinsumDesc* __restrict__ gd,
+                                                          const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int K = (int)d.K, N = (int)d.N;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [N][K]
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int n = e / K, k = e % K;
+    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  }
+  __syncthreads();
+  const int64_t V = d.V;
+  const int64_t vstride = d.m_sa[d.nm - 1];
+  float amax = 0.f;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < d.M;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t vi = m % V, o = m / V;
+    const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
+    float2 a[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      a[k] = k < K ? a_row[decompose(k, d.nk, d.k_ext, d.k_sa)] : make_float2(0.f, 0.f);
+    for (int n = 0; n < N; ++n) {
+      float cr = 0.f, ci = 0.f;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k < K) {
+          const float2 b = Bs[n * K + k];
+          cr = fmaf(a[k].x, b.x, cr);
+          cr = fmaf(-a[k].y, b.y, cr);
+          ci = fmaf(a[k].x, b.y, ci);
+          ci = fmaf(a[k].y, b.x, ci);
+        }
+      }
+      store_out(d, (o * N + n) * V + vi, cr, ci, amax);
+    }
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
 // ---------------------------------------------------------------- SIMT einsum, split-K dot
 // Few outputs, long K (e.g. the last step of a closed network, a 2^30-long dot):
 // block b takes output p = b / nchunk and a kchunk range of k; fp64 block
@@ -377,6 +425,15 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     else if (h.N <= 16) einsum_skinny_kernel<16><<<g, th, smem, s>>>(d_desc, leaf_off);
     else if (h.N <= 32) einsum_skinny_kernel<32><<<g, th, smem, s>>>(d_desc, leaf_off);
     else einsum_skinny_kernel<64><<<g, th, smem, s>>>(d_desc, leaf_off);
+    return cudaGetLastError();
+  }
+  if (h.mode == 3) {
+    const size_t smem = sizeof(float2) * h.K * h.N;
+    const int g = grid_for(h.M, th);
+    if (h.K <= 2) einsum_wide_kernel<2><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else if (h.K <= 4) einsum_wide_kernel<4><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else if (h.K <= 8) einsum_wide_kernel<8><<<g, th, smem, s>>>(d_desc, leaf_off);
+    else einsum_wide_kernel<16><<<g, th, smem, s>>>(d_desc, leaf_off);
     return cudaGetLastError();
   }
   if (h.mode == 2) {

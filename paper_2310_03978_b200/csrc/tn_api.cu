@@ -99,6 +99,7 @@ struct tn_ctx {
   int num_sms = 148;
   // k-blocks per promoted TMEM chunk: 3-pass / 1-pass
   int kchunk3 = 1, kchunk1 = 0;
+  int group_m = 16;             // GEMM tile rasterization group (tile rows)
   // network
   bool loaded = false, pathed = false, planned = false;
   int n_tensors = 0;
@@ -295,6 +296,8 @@ tn_status build_plan(tn_ctx* c) {
   const int skinny_big = env_int("TN_SKINNY_MIN_BIG", 1024);
   const int dot_min_k = env_int("TN_DOT_MIN_K", 4096);
   const int dot_max_out = env_int("TN_DOT_MAX_OUT", 4096);
+  const int tc_deep_k = env_int("TN_TC_DEEP_K", 1024);
+  const int skinny_max_small = env_int("TN_SKINNY_MAX_SMALL", 64);
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
 
@@ -397,7 +400,11 @@ tn_status build_plan(tn_ctx* c) {
     c->peak = std::max(c->peak, (double)out_elems);
 
     const int64_t big = std::max(sp.m, sp.n), small = std::min(sp.m, sp.n);
-    sp.tc = !disable_tc && big >= tc_big && small >= tc_small && sp.k >= tc_k && !sp.final_step &&
+    // tensor cores for GEMM-shaped steps; a deep K (>= tc_deep_k) keeps a step on the
+    // tensor cores even with a narrow side: it is bound by streaming the big operand
+    // once, which the TMA pipeline does at HBM speed (padding N only costs MMA slots).
+    sp.tc = !disable_tc && big >= tc_big && sp.k >= tc_k &&
+            (small >= tc_small || sp.k >= tc_deep_k) && !sp.final_step &&
             sp.m < INT32_MAX && sp.n < INT32_MAX && sp.k < INT32_MAX && sp.J < INT32_MAX;
     sp.swap = sp.tc && sp.n > sp.m;   // tensor-core M side = larger free extent
 
@@ -406,7 +413,7 @@ tn_status build_plan(tn_ctx* c) {
     if (!sp.tc) {
       const int64_t outs = sp.J * sp.m * sp.n;
       auto skinny = [&](int64_t big, int64_t small) {
-        return big >= skinny_big && small <= 64 && small * sp.k <= 8192 && sp.k <= 256;
+        return big >= skinny_big && small <= skinny_max_small && small * sp.k <= 8192 && sp.k <= 256;
       };
       const bool one_batch = !sp.merge || sp.J == 1;   // J = 1 merges fold their slabs
       if (outs <= dot_max_out && sp.k >= dot_min_k) {
@@ -418,10 +425,22 @@ tn_status build_plan(tn_ctx* c) {
       } else if (one_batch && skinny(sp.n, sp.m)) {
         sp.mode = 1;
         sp.x_is_b = true;
+      } else if (one_batch) {
+        // wide skinny: outer-product-like (k <= 16), small side up to 4096
+        auto wide = [&](int64_t big, int64_t small) {
+          return big >= skinny_big && big >= small && small * sp.k <= 8192 && sp.k <= 16;
+        };
+        if (wide(sp.m, sp.n)) {
+          sp.mode = 3;
+          sp.x_is_b = false;
+        } else if (wide(sp.n, sp.m)) {
+          sp.mode = 3;
+          sp.x_is_b = true;
+        }
       }
     }
     std::vector<VDim> od;
-    if (sp.mode == 1) {
+    if (sp.mode == 1 || sp.mode == 3) {
       // output [X outer dims][Y dims][v], v = the big operand's smallest-stride dim
       const auto& X = sp.x_is_b ? FB : FA;
       const auto& Y = sp.x_is_b ? FA : FB;
@@ -615,7 +634,7 @@ tn_status build_plan(tn_ctx* c) {
       return fail(TN_ERR_INTERNAL, "step " + std::to_string(s) + ": too many non-coalescable dims");
     unsigned* absmax_out = sp.final_step ? nullptr : c->d_absmax + (n_leaves + s);
     float2* Cptr = sp.final_step ? nullptr : c->d_arena + sp.out_off;
-    if (!sp.tc && sp.mode == 1) {
+    if (!sp.tc && (sp.mode == 1 || sp.mode == 3)) {
       // skinny: X = big operand (streamed), Y = small operand (smem); out [Xo][Y][v]
       const View& XV = sp.x_is_b ? B : A;
       const View& YV = sp.x_is_b ? A : B;
@@ -635,7 +654,7 @@ tn_status build_plan(tn_ctx* c) {
         return fail(TN_ERR_INTERNAL, "step " + std::to_string(s) + ": too many dims (skinny)");
       tn::EinsumDesc& e = eds[sp.einsum_idx];
       memset(&e, 0, sizeof(e));
-      e.mode = 1;
+      e.mode = sp.mode;
       e.A = base_of(XV); e.B = base_of(YV); e.C = Cptr;
       e.a_off = XV.off; e.b_off = YV.off;
       if (sp.merge) {   // J == 1: fold the single slab of each side into the offsets
@@ -812,6 +831,7 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
         }
         tn::GemmArgs ga = sp.gemm;
         ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
+        ga.group_m = c->group_m;
         Timer tm(c, 0, sp.tcc, sp.tmc);
         TN_CUDA(tn::launch_gemm(ga, ps, c->num_sms, sm));
       }
@@ -954,6 +974,7 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   c->num_sms = prop.multiProcessorCount;
   c->kchunk3 = env_int("TN_KCHUNK3", 1);
   c->kchunk1 = env_int("TN_KCHUNK1", 0);
+  c->group_m = env_int("TN_GEMM_GROUP", 16);
   *out = c;
   return TN_OK;
 }
@@ -1318,7 +1339,11 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     g.tiles_n = (int32_t)((n + 127) / 128);
     g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * J;
     g.kchunk = passes == 3 ? c->kchunk3 : c->kchunk1;
-    TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));
+    g.group_m = c->group_m;
+    {
+      Timer tm(c, 0, 8.0 * (double)J * m * n * k, 8.0 * (double)(ga * m * k + gb * n * k + J * m * n));
+      TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));
+    }
     cudaError_t e = cudaStreamSynchronize(sm);
     cudaFree(dp);
     cudaFree(scr);

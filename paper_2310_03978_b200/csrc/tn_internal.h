@@ -66,6 +66,7 @@ struct GemmArgs {
   int64_t n_tiles;
   int32_t kchunk;                 // k-blocks per TMEM chunk promoted to the fp32 RN
                                   // register sum (0 = whole K in TMEM); see DESIGN.md
+  int32_t group_m;                // tile rasterization: tile rows per group (L2 reuse)
 };
 
 // ---------------------------------------------------------------- slice select

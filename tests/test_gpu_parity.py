@@ -122,7 +122,10 @@ ROUTES = {
     "simt": {"TN_DISABLE_TC": "1"},
     "simt_modes": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_DOT_MIN_K": "2",
                    "TN_DOT_MAX_OUT": "16"},
+    "simt_wide": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SKINNY_MAX_SMALL": "0"},
     "tc": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2"},
+    "tc_deep": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "100000", "TN_TC_MIN_K": "2",
+                "TN_TC_DEEP_K": "4"},
     "default": {},
 }
 
@@ -135,13 +138,13 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
     w = configs.small(grid=(3, 4), cycles=8, mode=mode, n_samples=64, n_slices=8, seed=2)
     ref = oracle.contract(w.net, w.path, w.sliced, w.samples)
     out, info = run_gpu(ctx, w)
-    if route == "tc":
+    if route in ("tc", "tc_deep"):
         assert info["n_tc_steps"] > 0
-    if route == "simt_modes":
+    if route in ("simt_modes", "simt_wide"):
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
         modes = {s["mode"] for s in c.plan_json()["steps"]}
-        assert {1, 2} <= modes, modes
+        assert ({1, 2} if route == "simt_modes" else {3}) <= modes, modes
     assert rel_l2(out, ref) <= EXT_TOL
     out_m, _ = run_gpu(ctx, w, precision="mixed", topk=10)
     assert rel_l2(out_m, ref) <= MIX_TOL
@@ -201,18 +204,22 @@ def test_c4_bench_workload_sampled_subslice(ctx):
     sub-slice of slice 0 compared element-by-element with the oracle (the oracle
     cannot afford a whole 3e14-flop slice), plus the slicing identity on GPU:
     a coarse slice equals the sum of its sub-slices."""
+    from tnworkloads.network import fix_bonds
     w = configs.c4()
-    fine, pc = _refine(w, 4e11)
-    extra = len(fine) - len(w.sliced)
+    fine, pc = _refine(w, 3e11)
+    extra = fine[len(w.sliced):]
+    # carve the sub-slice as a sub-network (extra bonds fixed to 0): the slice count of
+    # the refined slicing would overflow int64, the sub-network keeps the bench's slices
+    sub = fix_bonds(w.net, {x: 0 for x in extra})
     c = Contraction(device=0, stream=torch.cuda.current_stream())
-    c.setup(w.net, w.samples, w.path, fine)
+    c.setup(sub, w.samples, w.path, w.sliced)
     c.contract(0, 1)
     got = c.sum_slices_host()
     info = c.info()
     c.close()
-    ref = oracle.contract_slice(w.net, w.path, fine, 0, w.samples)
+    ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
     err = rel_l2(got, ref)
-    print(f"C4 sub-slice: extra bonds {extra}, T_cc {pc.flops_per_slice:.3g}, "
+    print(f"C4 sub-slice: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
           f"tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}")
     assert err <= EXT_TOL
 

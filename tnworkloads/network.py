@@ -60,6 +60,24 @@ class Network:
         return cnt
 
 
+def fix_bonds(net: Network, values: dict) -> Network:
+    """Sub-network with closed bonds fixed to given values (index selection on the
+    two tensors carrying each bond; tensor ids unchanged, so a path stays valid).
+    Used to carve oracle-sized samples out of a large workload for parity tests."""
+    tensors, labels = [], []
+    for t, ls in zip(net.tensors, net.labels):
+        t = np.asarray(t)
+        ls = list(ls)
+        for x in [x for x in ls if x in values]:
+            ax = ls.index(x)
+            t = np.take(t, values[x], axis=ax)
+            ls.pop(ax)
+        tensors.append(np.ascontiguousarray(t))
+        labels.append(ls)
+    dims = {x: d for x, d in net.dims.items() if x not in values}
+    return Network(tensors, labels, dims, list(net.open_labels), net.n_qubits, net.coords)
+
+
 def circuit_to_network(c: Circuit, simplify: bool = True) -> Network:
     if simplify:
         return _simplified(c)
