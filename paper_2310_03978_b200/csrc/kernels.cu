@@ -414,9 +414,37 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, const
   return cudaGetLastError();
 }
 
+template <typename F>
+cudaError_t allow_big_smem(F* kern) {
+  // the staged small operand can exceed the 48 KB default dynamic smem window
+  static_assert(sizeof(F*) > 0, "");
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+}
+
+cudaError_t enable_einsum_smem() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<4>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<8>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<16>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<32>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<64>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_wide_kernel<2>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_wide_kernel<4>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_wide_kernel<8>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_wide_kernel<16>)) != cudaSuccess) return e;
+  done = true;
+  return cudaSuccess;
+}
+
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off,
                           cudaStream_t s) {
   const int th = 256;
+  if (h.mode == 1 || h.mode == 3) {
+    cudaError_t e = enable_einsum_smem();
+    if (e != cudaSuccess) return e;
+  }
   if (h.mode == 1) {
     const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
     const int g = grid_for(h.M, th);

@@ -75,7 +75,10 @@ struct StepPlan {
   int in_slot[2] = {0, 0};
   int mode = 0;                 // SIMT mode: 0 general, 1 skinny, 2 split-K dot
   bool x_is_b = false;          // skinny: the big (streamed) operand is B
-  int64_t vlabel = 0;           // skinny: label of the lane (vector) dim
+  std::vector<int64_t> vlabels; // skinny: labels of the lane (vector) run, outer -> inner
+  // output label order chosen by the planner (consumer look-ahead): order1 = P side
+  // (tensor cores) / A side (SIMT general) / X outer dims (skinny); order2 = Q / B / Y
+  std::vector<int64_t> order1, order2;
   tn::EinsumDesc hdesc;         // host copy of the SIMT descriptor (launch parameters)
 };
 
@@ -245,6 +248,16 @@ void coalesce2(std::vector<KDim>& d) {
   d.swap(o);
 }
 
+// dims reordered to follow `order` (labels; every dim's label appears once in it)
+std::vector<VDim> arrange(const std::vector<VDim>& d, const std::vector<int64_t>& order) {
+  std::vector<VDim> o;
+  o.reserve(d.size());
+  for (int64_t l : order)
+    for (auto& x : d)
+      if (x.label == l) { o.push_back(x); break; }
+  return o;
+}
+
 void contiguous_strides(std::vector<VDim>& d) {
   int64_t s = 1;
   for (int p = (int)d.size() - 1; p >= 0; --p) {
@@ -324,6 +337,40 @@ tn_status build_plan(tn_ctx* c) {
     v.absmax_slot = t;
     live[t] = v;
   }
+
+  // Consumer look-ahead (index reordering, §4.1, generalised to
+  // every step): for each step's output, the bonds its consumer will contract.
+  // Producers place those bonds last (sorted), so the consumer's operand prep
+  // reads long contiguous runs.
+  std::vector<std::unordered_set<int64_t>> consumer_k(n_steps);
+  {
+    std::vector<std::unordered_set<int64_t>> lab(n_leaves);
+    std::vector<int> producer(n_leaves, -1);
+    for (int t = 0; t < n_leaves; ++t)
+      for (auto& d : live[t].dims)
+        if (d.label != GROUP) lab[t].insert(d.label);
+    for (int s = 0; s < n_steps; ++s) {
+      const int i = c->path[s].first, j = c->path[s].second;
+      std::unordered_set<int64_t> shared;
+      for (int64_t x : lab[i]) if (lab[j].count(x)) shared.insert(x);
+      if (producer[i] >= 0) consumer_k[producer[i]] = shared;
+      if (producer[j] >= 0) consumer_k[producer[j]] = shared;
+      std::unordered_set<int64_t> out;
+      for (int64_t x : lab[i]) if (!shared.count(x)) out.insert(x);
+      for (int64_t x : lab[j]) if (!shared.count(x)) out.insert(x);
+      lab[i] = out;
+      lab[j].clear();
+      producer[i] = s;
+    }
+  }
+  // stable partition: bonds the consumer keeps first, bonds it contracts last (sorted)
+  auto consumer_order = [](std::vector<VDim>& d, const std::unordered_set<int64_t>& kc) {
+    std::vector<VDim> keep, con;
+    for (auto& x : d) (kc.count(x.label) ? con : keep).push_back(x);
+    std::sort(con.begin(), con.end(), [](const VDim& a, const VDim& b) { return a.label < b.label; });
+    keep.insert(keep.end(), con.begin(), con.end());
+    d.swap(keep);
+  };
 
   Arena arena;
   std::vector<int32_t> tables;
@@ -440,24 +487,46 @@ tn_status build_plan(tn_ctx* c) {
       }
     }
     std::vector<VDim> od;
+    const auto& kc = consumer_k[s];
     if (sp.mode == 1 || sp.mode == 3) {
       // output [X outer dims][Y dims][v], v = the big operand's smallest-stride dim
       const auto& X = sp.x_is_b ? FB : FA;
-      const auto& Y = sp.x_is_b ? FA : FB;
+      std::vector<VDim> Y = sp.x_is_b ? FA : FB;
+      // lane dims v: the contiguous run of X's memory that starts at its smallest
+      // stride (lanes then read consecutive addresses); kept innermost in the output
+      std::vector<int> vrun;
       int vi = -1;
       for (int p = 0; p < (int)X.size(); ++p)
         if (X[p].ext > 1 && (vi < 0 || X[p].stride < X[vi].stride)) vi = p;
-      sp.vlabel = X[vi].label;
+      vrun.push_back(vi);
+      for (int64_t next = X[vi].stride * X[vi].ext;;) {
+        int q = -1;
+        for (int p = 0; p < (int)X.size(); ++p)
+          if (X[p].ext > 1 && X[p].stride == next &&
+              std::find(vrun.begin(), vrun.end(), p) == vrun.end()) q = p;
+        if (q < 0) break;
+        vrun.push_back(q);
+        next *= X[q].ext;
+      }
+      sp.vlabels.clear();
+      for (int r = (int)vrun.size() - 1; r >= 0; --r) sp.vlabels.push_back(X[vrun[r]].label);
+      std::vector<VDim> Xo;
       for (int p = 0; p < (int)X.size(); ++p)
-        if (p != vi) od.push_back({X[p].label, X[p].ext, 0});
-      for (auto& d : Y) od.push_back({d.label, d.ext, 0});
-      od.push_back({X[vi].label, X[vi].ext, 0});
+        if (std::find(vrun.begin(), vrun.end(), p) == vrun.end()) Xo.push_back(X[p]);
+      consumer_order(Xo, kc);
+      consumer_order(Y, kc);
+      for (auto& d : Xo) { od.push_back({d.label, d.ext, 0}); sp.order1.push_back(d.label); }
+      for (auto& d : Y) { od.push_back({d.label, d.ext, 0}); sp.order2.push_back(d.label); }
+      for (int r = (int)vrun.size() - 1; r >= 0; --r)
+        od.push_back({X[vrun[r]].label, X[vrun[r]].ext, 0});
     } else {
       if (sp.merge) od.push_back({GROUP, sp.J, 0});
-      const auto& P = sp.swap ? FB : FA;
-      const auto& Q = sp.swap ? FA : FB;
-      for (auto& d : P) od.push_back({d.label, d.ext, 0});
-      for (auto& d : Q) od.push_back({d.label, d.ext, 0});
+      std::vector<VDim> P = sp.swap ? FB : FA;
+      std::vector<VDim> Q = sp.swap ? FA : FB;
+      consumer_order(P, kc);
+      consumer_order(Q, kc);
+      for (auto& d : P) { od.push_back({d.label, d.ext, 0}); sp.order1.push_back(d.label); }
+      for (auto& d : Q) { od.push_back({d.label, d.ext, 0}); sp.order2.push_back(d.label); }
     }
     contiguous_strides(od);
     out.dims = od;
@@ -627,6 +696,10 @@ tn_status build_plan(tn_ctx* c) {
     }
     const std::vector<VDim> FA0 = FA, FB0 = FB;
     const std::vector<KDim> K0 = K;
+    if (sp.mode != 1 && sp.mode != 3) {   // the planner's output order (consumer look-ahead)
+      FA = arrange(FA, sp.swap ? sp.order2 : sp.order1);
+      FB = arrange(FB, sp.swap ? sp.order1 : sp.order2);
+    }
     coalesce1(FA);
     coalesce1(FB);
     coalesce2(K);
@@ -640,11 +713,18 @@ tn_status build_plan(tn_ctx* c) {
       const View& YV = sp.x_is_b ? A : B;
       const auto& X0 = sp.x_is_b ? FB0 : FA0;
       std::vector<VDim> Xo, Ys = sp.x_is_b ? FA0 : FB0;
-      VDim v{0, 1, 0};
+      // merged lane dim: the run is contiguous in X and innermost (same order) in C
+      VDim v{0, 1, INT64_MAX};
       for (auto& d : X0) {
-        if (d.label == sp.vlabel) v = d;
-        else Xo.push_back(d);
+        if (std::find(sp.vlabels.begin(), sp.vlabels.end(), d.label) != sp.vlabels.end()) {
+          v.ext *= d.ext;
+          v.stride = std::min(v.stride, d.stride);
+        } else {
+          Xo.push_back(d);
+        }
       }
+      Xo = arrange(Xo, sp.order1);
+      Ys = arrange(Ys, sp.order2);
       coalesce1(Xo);
       coalesce1(Ys);
       std::vector<KDim> Kx = K0;
@@ -974,7 +1054,7 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   c->num_sms = prop.multiProcessorCount;
   c->kchunk3 = env_int("TN_KCHUNK3", 1);
   c->kchunk1 = env_int("TN_KCHUNK1", 0);
-  c->group_m = env_int("TN_GEMM_GROUP", 16);
+  c->group_m = env_int("TN_GEMM_GROUP", 8);   // best of {1,8,16,32} on 8192^2 x 16384
   *out = c;
   return TN_OK;
 }

@@ -224,6 +224,31 @@ def test_c4_bench_workload_sampled_subslice(ctx):
     assert err <= EXT_TOL
 
 
+@pytest.mark.timeout(900)
+def test_c3_sparse_state_sampled_subnetwork(ctx):
+    """Sparse-state boundary at full width (Sycamore-53 m=14, 2^16 samples): the
+    gather-batched (Eq. 7) merges run with J in the thousands; one slice of a
+    sub-network (extra bonds fixed) vs the oracle, all 2^16 amplitudes."""
+    from tnworkloads.network import fix_bonds
+    w = configs.c3()
+    fine, pc = _refine(w, 2e11)
+    extra = fine[len(w.sliced):]
+    sub = fix_bonds(w.net, {x: 0 for x in extra})
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(sub, w.samples, w.path, w.sliced)
+    pj = c.plan_json()
+    c.contract(0, 1)
+    got = c.sum_slices_host()
+    c.close()
+    ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
+    err = rel_l2(got, ref)
+    maxJ = max(s["J"] for s in pj["steps"])
+    print(f"C3 sub-network: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
+          f"max J {maxJ}, rel_l2 {err:.3e}")
+    assert maxJ > 1000
+    assert err <= EXT_TOL
+
+
 def test_c2_sampled_slices_at_full_size(ctx):
     """C2 at full size (30 q, 2^10 amplitudes, the 64-slice plan the bench times):
     a GPU slice equals the sum of its GPU sub-slices (slicing identity, any size),

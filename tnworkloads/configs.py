@@ -123,6 +123,25 @@ def c4(boundary: str = "single", peak: int = 32, tag: str = "a64") -> Workload:
     return w
 
 
+def c3(samples_log2: int = 16, peak: int = 30, tag: str = "a64") -> Workload:
+    """C3: Sycamore-53 m=14 with a sparse-state boundary of 2^samples_log2 uniform
+    random bitstrings (stand-ins for experiment samples, L501) — the sparse einsum
+    (Eq. 7) at scale: gather-batched merges with J up to ~2^16.  Cached order file
+    from tools/make_orders.py (sparse-aware U(Q) size model)."""
+    w = c4_base(f"sparse{samples_log2}", cycles=14)
+    fn = _order_file(f"c3_sparse{samples_log2}_p{peak}{tag}")
+    if not os.path.exists(fn):
+        raise FileNotFoundError(f"{fn} missing: run tools/make_orders.py c3 --cycles 14 "
+                                f"--boundary sparse{samples_log2} --peak {peak} --tag {tag}")
+    with open(fn) as f:
+        d = json.load(f)
+    w.path = [tuple(p) for p in d["path"]]
+    w.sliced = list(d["sliced"])
+    w.meta.update(d.get("meta", {}))
+    w.name = f"c3_sycamore53_m14_sparse{samples_log2}_p{peak}{tag}"
+    return w
+
+
 def small(grid=(3, 3), cycles=6, mode="sparse", n_samples=16, n_slices=4, seed=0,
           simplify=True) -> Workload:
     """Small seeded case for parity tests (oracle finishes in well under a second)."""

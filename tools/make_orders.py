@@ -26,8 +26,9 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.0,
                     help="Eq. 6 memory weight (flop-equivalents per byte of T_mc)")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--cycles", type=int, default=18)
     args = ap.parse_args()
-    w = configs.c4_base(boundary=args.boundary)
+    w = configs.c4_base(boundary=args.boundary, cycles=args.cycles)
     best = None
     for s in range(args.seeds):
         t = time.time()
