@@ -67,23 +67,54 @@ __global__ void slice_select_kernel(const SliceDesc* __restrict__ d) {
 }
 
 // ---------------------------------------------------------------- operand prep
-template <int PLANES>
-__global__ void __launch_bounds__(256) prep_kernel(const PrepDesc* __restrict__ gd,
-                                                   const int64_t* __restrict__ leaf_off,
-                                                   int64_t total) {
-  __shared__ __align__(16) PrepDesc d;
-  copy_desc_to_smem(&d, gd);
-  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+// Power-of-two exponent s with absmax·2^s in [2^14, 2^15) (inside the fp16 range,
+// PAPER.md L403 "dynamic scaling"); block 0 publishes it for the GEMM epilogue.
+__device__ __forceinline__ float prep_scale(const PrepDesc& d) {
   const float amax = __uint_as_float(*d.absmax_in);
   int s = 0;
   if (amax > 0.f) {
     int e;
     frexpf(amax, &e);            // amax = f * 2^e, f in [0.5, 1)
-    s = 15 - e;                  // amax * 2^s in [2^14, 2^15): inside fp16 range
+    s = 15 - e;
     s = max(-120, min(120, s));
   }
-  const float scale = ldexpf(1.0f, s);
   if (blockIdx.x == 0 && threadIdx.x == 0) *d.scale_out = s;
+  return ldexpf(1.0f, s);
+}
+
+// RN hi/lo split of 8 consecutive k-values (Eq. 8: big = rn(x), small = rn(x - big))
+// stored as one 16-byte vector per plane.
+template <int PLANES>
+__device__ __forceinline__ void split_store8(const PrepDesc& d, int64_t idx, const float2* v,
+                                             float scale) {
+  __align__(16) __half hr[8], hi[8], lr[8], li[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float xr = v[j].x * scale, xi = v[j].y * scale;
+    hr[j] = __float2half_rn(xr);
+    hi[j] = __float2half_rn(xi);
+    if (PLANES == 4) {
+      lr[j] = __float2half_rn(xr - __half2float(hr[j]));
+      li[j] = __float2half_rn(xi - __half2float(hi[j]));
+    }
+  }
+  const int64_t plane = d.plane_elems;
+  *reinterpret_cast<uint4*>(d.dst + idx) = *reinterpret_cast<const uint4*>(hr);
+  *reinterpret_cast<uint4*>(d.dst + plane + idx) = *reinterpret_cast<const uint4*>(hi);
+  if (PLANES == 4) {
+    *reinterpret_cast<uint4*>(d.dst + 2 * plane + idx) = *reinterpret_cast<const uint4*>(lr);
+    *reinterpret_cast<uint4*>(d.dst + 3 * plane + idx) = *reinterpret_cast<const uint4*>(li);
+  }
+}
+
+template <int PLANES>
+__global__ void __launch_bounds__(256, 4) prep_kernel(const PrepDesc* __restrict__ gd,
+                                                      const int64_t* __restrict__ leaf_off,
+                                                      int64_t total) {
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  const float scale = prep_scale(d);
   const int64_t plane = d.plane_elems;
   // Tiled transpose: a tile is TR rows x TK k-values of one slab.  Row and column
   // source offsets are decomposed once per tile into smem, so each element costs
@@ -181,6 +212,52 @@ __device__ __forceinline__ void store_out(const EinsumDesc& d, int64_t idx, doub
   amax = fmaxf(amax, fmaxf(fabsf((float)cr), fabsf((float)ci)));
 }
 
+// ---------------------------------------------------------------- operand prep, direct
+// Source walks k fastest (the common case once producers place the consumer's
+// contracted bonds last): no smem transpose.  A thread owns 8 consecutive k of one
+// row: 64 B of reads (16-B vectors when the innermost k dim is contiguous) and
+// one 16-B store per plane; neighbouring threads take neighbouring k groups.
+template <int PLANES>
+__global__ void __launch_bounds__(256, 4) prep_direct_kernel(const PrepDesc* __restrict__ gd,
+                                                             const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  const float scale = prep_scale(d);
+  const int64_t kgs = d.Kpad / 8;                      // Kpad is a multiple of 8
+  const int64_t total = d.G * d.R * kgs;
+  const bool kvec = d.nk > 0 && d.k_s[d.nk - 1] == 1 && (d.k_ext[d.nk - 1] % 8) == 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kg = w % kgs, rg = w / kgs;
+    const int64_t r = rg % d.R, g = rg / d.R;
+    const int64_t k0 = kg * 8;
+    const int64_t base = g * d.g_stride + decompose(r, d.nr, d.r_ext, d.r_s);
+    float2 v[8];
+    if (kvec && k0 + 8 <= d.K) {
+      const float2* p = src + base + decompose(k0, d.nk, d.k_ext, d.k_s);
+      if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 q = reinterpret_cast<const float4*>(p)[j];
+          v[2 * j] = make_float2(q.x, q.y);
+          v[2 * j + 1] = make_float2(q.z, q.w);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = p[j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t k = k0 + j;
+        v[j] = k < d.K ? src[base + decompose(k, d.nk, d.k_ext, d.k_s)] : make_float2(0.f, 0.f);
+      }
+    }
+    split_store8<PLANES>(d, rg * d.Kpad + k0, v, scale);
+  }
+}
+
 // ---------------------------------------------------------------- SIMT einsum, general
 // One thread per output C[j][m][n]; fp64 accumulation (a long fp32 RN chain would
 // cost ~2^-24·sqrt(K/2) relative).
@@ -248,33 +325,54 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
   __syncthreads();
   const int64_t V = d.V;
   const int64_t vstride = d.m_sa[d.nm - 1];
-  const int64_t Mo = d.M / V;
+  // U rows per thread per iteration (independent loads in flight); U = 2 while
+  // the accumulators fit comfortably in registers
+  constexpr int U = NMAX <= 16 ? 2 : 1;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
   float amax = 0.f;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < d.M;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = m % V, o = m / V;
-    const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
-    float accr[NMAX], acci[NMAX];
+  for (int64_t m0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m0 < d.M; m0 += U * step) {
+    const float2* a_row[U];
+    int64_t obase[U];
+    bool live[U];
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) { accr[n] = 0.f; acci[n] = 0.f; }
+    for (int u = 0; u < U; ++u) {
+      const int64_t m = m0 + u * step;
+      live[u] = m < d.M;
+      const int64_t mm = live[u] ? m : m0;
+      const int64_t vi = mm % V, o = mm / V;
+      a_row[u] = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
+      obase[u] = o * N * V + vi;
+    }
+    float accr[U][NMAX], acci[U][NMAX];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) { accr[u][n] = 0.f; acci[u][n] = 0.f; }
     for (int k = 0; k < K; ++k) {
-      const float2 a = a_row[koff[k]];
+      float2 a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = a_row[u][koff[k]];
 #pragma unroll
       for (int n = 0; n < NMAX; ++n) {
         if (n < N) {
           const float2 b = Bs[k * N + n];
-          accr[n] = fmaf(a.x, b.x, accr[n]);
-          accr[n] = fmaf(-a.y, b.y, accr[n]);
-          acci[n] = fmaf(a.x, b.y, acci[n]);
-          acci[n] = fmaf(a.y, b.x, acci[n]);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            accr[u][n] = fmaf(a[u].x, b.x, accr[u][n]);
+            accr[u][n] = fmaf(-a[u].y, b.y, accr[u][n]);
+            acci[u][n] = fmaf(a[u].x, b.y, acci[u][n]);
+            acci[u][n] = fmaf(a[u].y, b.x, acci[u][n]);
+          }
         }
       }
     }
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n)
-      if (n < N) store_out(d, (o * N + n) * V + vi, accr[n], acci[n], amax);
+    for (int u = 0; u < U; ++u)
+      if (live[u])
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+          if (n < N) store_out(d, obase[u] + (int64_t)n * V, accr[u][n], acci[u][n], amax);
   }
-  (void)Mo;
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
@@ -404,9 +502,17 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, const int64_t* leaf_off,
-                        cudaStream_t s) {
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int r_fast,
+                        const int64_t* leaf_off, cudaStream_t s) {
   const int th = 256;
+  if (!r_fast) {   // k-walking source: direct kernel, 8 elements per thread
+    const int g = grid_for(total / 8, th);
+    if (planes == 4)
+      prep_direct_kernel<4><<<g, th, 0, s>>>(d_desc, leaf_off);
+    else
+      prep_direct_kernel<2><<<g, th, 0, s>>>(d_desc, leaf_off);
+    return cudaGetLastError();
+  }
   if (planes == 4)
     prep_kernel<4><<<grid_for(total, th), th, 0, s>>>(d_desc, leaf_off, total);
   else

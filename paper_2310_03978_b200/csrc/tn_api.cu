@@ -73,6 +73,7 @@ struct StepPlan {
   int64_t prep_total[2] = {0, 0};
   int64_t R[2] = {0, 0}, Kpad = 0, G[2] = {1, 1};
   int in_slot[2] = {0, 0};
+  int r_fast[2] = {0, 0};       // prep: source walks rows (transposer) vs k (direct)
   int mode = 0;                 // SIMT mode: 0 general, 1 skinny, 2 split-K dot
   bool x_is_b = false;          // skinny: the big (streamed) operand is B
   std::vector<int64_t> vlabels; // skinny: labels of the lane (vector) run, outer -> inner
@@ -811,6 +812,7 @@ tn_status build_plan(tn_ctx* c) {
           const int64_t rs = p.nr ? p.r_s[p.nr - 1] : INT64_MAX;
           const int64_t ks = p.nk ? p.k_s[p.nk - 1] : INT64_MAX;
           p.read_r_fast = rs < ks ? 1 : 0;
+          sp.r_fast[side] = p.read_r_fast;
         }
         int64_t off0 = 0;
         int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
@@ -907,7 +909,7 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
         for (int side = 0; side < 2; ++side) {
           Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes));
           TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
-                                  c->d_leaf_off, sm));
+                                  sp.r_fast[side], c->d_leaf_off, sm));
         }
         tn::GemmArgs ga = sp.gemm;
         ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
@@ -1408,8 +1410,8 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     TN_CUDA(cudaMalloc(&dp, sizeof(p)));
     TN_CUDA(cudaMemcpyAsync(dp, p, sizeof(p), cudaMemcpyHostToDevice, sm));
     const int planes = passes == 3 ? 4 : 2;
-    TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, nullptr, sm));
-    TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, nullptr, sm));
+    TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, 0, nullptr, sm));
+    TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, 0, nullptr, sm));
     g.J = (int32_t)J; g.M = (int32_t)m; g.N = (int32_t)n; g.K = (int32_t)k;
     g.ia = ia; g.ib = ib;
     g.C = reinterpret_cast<float2*>(C);

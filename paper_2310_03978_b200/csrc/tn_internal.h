@@ -83,7 +83,7 @@ struct SliceDesc {
 
 // kernel launchers (kernels.cu / gemm_tcgen05.cu)
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
-cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes,
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int r_fast,
                         const int64_t* leaf_off, cudaStream_t s);
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
                           const int64_t* leaf_off, cudaStream_t s);
