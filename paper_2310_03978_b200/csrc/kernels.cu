@@ -10,6 +10,8 @@
 //   gather_out    — a9: merged-configuration order -> caller sample order
 #include "tn_internal.h"
 
+#include <algorithm>
+
 namespace tn {
 
 namespace {
@@ -258,6 +260,56 @@ __global__ void __launch_bounds__(256, 4) prep_direct_kernel(const PrepDesc* __r
   }
 }
 
+// ---------------------------------------------------------------- operand prep, general
+// Arbitrary permutation (cuTT-style): a tile is Bsz destination-contiguous
+// elements (k-run of the plane rows) x Asz source-contiguous elements; block
+// offset tables live in smem, so reads walk the source's innermost run and the
+// half2 plane stores walk the destination's, whatever the interleaving.
+template <int PLANES>
+__global__ void __launch_bounds__(256, 4) prep_gt_kernel(const PrepDesc* __restrict__ gd,
+                                                         const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  __shared__ int64_t srcA[64], dstA[64], srcB[64], dstB[64];
+  __shared__ float2 tile[64][33];                     // [b][a], a <= 32
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  const float scale = prep_scale(d);
+  const int As = d.Asz, Bs = d.Bsz;
+  if (threadIdx.x < As) {
+    srcA[threadIdx.x] = decompose(threadIdx.x, d.na, d.a_ext, d.a_src);
+    dstA[threadIdx.x] = decompose(threadIdx.x, d.na, d.a_ext, d.a_dst);
+  } else if (threadIdx.x >= 64 && threadIdx.x - 64 < Bs) {
+    const int b = threadIdx.x - 64;
+    srcB[b] = decompose(b, d.nb, d.b_ext, d.b_src);
+    dstB[b] = decompose(b, d.nb, d.b_ext, d.b_dst);
+  }
+  const int64_t plane = d.plane_elems;
+  for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
+    const int64_t sc = decompose(c, d.nc, d.c_ext, d.c_src);
+    const int64_t dc = decompose(c, d.nc, d.c_ext, d.c_dst);
+    __syncthreads();   // offset tables ready / previous tile consumed
+    for (int e = threadIdx.x; e < As * Bs; e += blockDim.x) {
+      const int a = e % As, b = e / As;
+      tile[b][a] = src[sc + srcA[a] + srcB[b]];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < As * Bs / 2; e += blockDim.x) {
+      const int b = (e % (Bs / 2)) * 2, a = e / (Bs / 2);
+      const float2 v0 = tile[b][a], v1 = tile[b + 1][a];
+      const float xr0 = v0.x * scale, xi0 = v0.y * scale, xr1 = v1.x * scale, xi1 = v1.y * scale;
+      const __half2 hr = __floats2half2_rn(xr0, xr1), hi = __floats2half2_rn(xi0, xi1);
+      const int64_t idx = dc + dstA[a] + dstB[b];     // dstB[b+1] = dstB[b] + 1, idx even
+      reinterpret_cast<__half2*>(d.dst + idx)[0] = hr;
+      reinterpret_cast<__half2*>(d.dst + plane + idx)[0] = hi;
+      if (PLANES == 4) {
+        const float2 fr = __half22float2(hr), fi = __half22float2(hi);
+        reinterpret_cast<__half2*>(d.dst + 2 * plane + idx)[0] = __floats2half2_rn(xr0 - fr.x, xr1 - fr.y);
+        reinterpret_cast<__half2*>(d.dst + 3 * plane + idx)[0] = __floats2half2_rn(xi0 - fi.x, xi1 - fi.y);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- SIMT einsum, general
 // One thread per output C[j][m][n]; fp64 accumulation (a long fp32 RN chain would
 // cost ~2^-24·sqrt(K/2) relative).
@@ -502,10 +554,19 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int r_fast,
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind,
                         const int64_t* leaf_off, cudaStream_t s) {
   const int th = 256;
-  if (!r_fast) {   // k-walking source: direct kernel, 8 elements per thread
+  if (kind == 2) {   // general transposer, 2048-element tiles
+    int64_t tiles = total / 2048;
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 8);
+    if (planes == 4)
+      prep_gt_kernel<4><<<g, th, 0, s>>>(d_desc, leaf_off);
+    else
+      prep_gt_kernel<2><<<g, th, 0, s>>>(d_desc, leaf_off);
+    return cudaGetLastError();
+  }
+  if (kind == 1) {   // k-walking source: direct kernel, 8 elements per thread
     const int g = grid_for(total / 8, th);
     if (planes == 4)
       prep_direct_kernel<4><<<g, th, 0, s>>>(d_desc, leaf_off);

@@ -73,7 +73,7 @@ struct StepPlan {
   int64_t prep_total[2] = {0, 0};
   int64_t R[2] = {0, 0}, Kpad = 0, G[2] = {1, 1};
   int in_slot[2] = {0, 0};
-  int r_fast[2] = {0, 0};       // prep: source walks rows (transposer) vs k (direct)
+  int r_fast[2] = {0, 0};       // prep kernel kind per side (choose_prep_kind)
   int mode = 0;                 // SIMT mode: 0 general, 1 skinny, 2 split-K dot
   bool x_is_b = false;          // skinny: the big (streamed) operand is B
   std::vector<int64_t> vlabels; // skinny: labels of the lane (vector) run, outer -> inner
@@ -104,6 +104,7 @@ struct tn_ctx {
   // k-blocks per promoted TMEM chunk: 3-pass / 1-pass
   int kchunk3 = 1, kchunk1 = 0;
   int group_m = 16;             // GEMM tile rasterization group (tile rows)
+  bool debug_plan = false;      // TN_DEBUG_PLAN=1: print operand layouts while planning
   // network
   bool loaded = false, pathed = false, planned = false;
   int n_tensors = 0;
@@ -259,6 +260,68 @@ std::vector<VDim> arrange(const std::vector<VDim>& d, const std::vector<int64_t>
   return o;
 }
 
+// Operand-prep kernel choice: 1 = direct (source walks k with a
+// contiguous innermost k run of >= 8), 2 = general transposer (blocks: the
+// destination's contiguous k-run x the source's innermost run), 0 = r/k tile
+// transposer (fallback).  Fills the general-transposer fields.
+int choose_prep_kind(tn::PrepDesc& p, int force) {
+  if (force == 0 || force == 1) return force;
+  if (force != 2 && p.nk > 0 && p.k_s[p.nk - 1] == 1 && p.k_ext[p.nk - 1] % 8 == 0) return 1;
+  if (p.K % 8 != 0 || p.Kpad != p.K || (force != 2 && p.G * p.R * p.K < 2048))
+    return p.read_r_fast ? 0 : 1;
+  struct D { int64_t e, s, t; };
+  std::vector<D> pool;
+  if (p.G > 1) pool.push_back({p.G, p.g_stride, p.R * p.Kpad});
+  int64_t t = p.Kpad;
+  for (int d = p.nr - 1; d >= 0; --d) { pool.push_back({p.r_ext[d], p.r_s[d], t}); t *= p.r_ext[d]; }
+  t = 1;
+  for (int d = p.nk - 1; d >= 0; --d) { pool.push_back({p.k_ext[d], p.k_s[d], t}); t *= p.k_ext[d]; }
+  // take a block of `target` elements from the pool, walking `key` (dst or src
+  // stride) upward; the last dim is split when it overshoots (power-of-two dims)
+  auto take = [&](int64_t target, bool by_dst, std::vector<D>& blk) -> int64_t {
+    int64_t size = 1;
+    while (size < target && !pool.empty()) {
+      int best = 0;
+      for (int q = 1; q < (int)pool.size(); ++q)
+        if ((by_dst ? pool[q].t : pool[q].s) < (by_dst ? pool[best].t : pool[best].s)) best = q;
+      D x = pool[best];
+      if (by_dst && x.t != size) break;             // destination block must stay contiguous
+      const int64_t need = (target + size - 1) / size;
+      if (x.e > need && x.e % need == 0) {
+        blk.push_back({need, x.s, x.t});
+        pool[best] = {x.e / need, x.s * need, x.t * need};
+        size *= need;
+      } else {
+        blk.push_back(x);
+        pool.erase(pool.begin() + best);
+        size *= x.e;
+      }
+    }
+    return size;
+  };
+  std::vector<D> B, A;
+  const int64_t bs = take(64, true, B);
+  const int64_t as = take(32, false, A);
+  if (bs % 2 != 0 || bs > 64 || as > 32 || (int)B.size() > 8 || (int)A.size() > 8 ||
+      (int)pool.size() > TN_MAXD)
+    return p.read_r_fast ? 0 : 1;
+  // block index order: row-major over the listed dims, so list them outer -> inner
+  std::reverse(B.begin(), B.end());
+  std::reverse(A.begin(), A.end());
+  p.nb = (int)B.size();
+  for (int i = 0; i < p.nb; ++i) { p.b_ext[i] = B[i].e; p.b_src[i] = B[i].s; p.b_dst[i] = B[i].t; }
+  p.na = (int)A.size();
+  for (int i = 0; i < p.na; ++i) { p.a_ext[i] = A[i].e; p.a_src[i] = A[i].s; p.a_dst[i] = A[i].t; }
+  p.nc = (int)pool.size();
+  p.nC = 1;
+  for (int i = 0; i < p.nc; ++i) {
+    p.c_ext[i] = pool[i].e; p.c_src[i] = pool[i].s; p.c_dst[i] = pool[i].t; p.nC *= pool[i].e;
+  }
+  p.Asz = (int32_t)as;
+  p.Bsz = (int32_t)bs;
+  return 2;
+}
+
 void contiguous_strides(std::vector<VDim>& d) {
   int64_t s = 1;
   for (int p = (int)d.size() - 1; p >= 0; --p) {
@@ -312,6 +375,7 @@ tn_status build_plan(tn_ctx* c) {
   const int dot_max_out = env_int("TN_DOT_MAX_OUT", 4096);
   const int tc_deep_k = env_int("TN_TC_DEEP_K", 1024);
   const int skinny_max_small = env_int("TN_SKINNY_MAX_SMALL", 64);
+  const int prep_force = env_int("TN_PREP_FORCE", -1);   // tests: force a prep kernel kind
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
 
@@ -591,11 +655,9 @@ tn_status build_plan(tn_ctx* c) {
   }
   c->arena_elems = arena.high;
   c->scratch_bytes = scratch;
-  if (c->host_only) {
-    c->planned = true;
-    return TN_OK;
-  }
-
+  if (c->sliced.size() > 64) return fail(TN_ERR_DATA, "at most 64 sliced bonds");
+  cudaStream_t sm = c->stream;
+  if (!c->host_only) {   // host-only planners build the descriptors below without CUDA
   // ------------------------------------------------------------ device buffers
   tn_status st;
   if ((st = dev_alloc(c, &c->d_arena, (size_t)std::max<int64_t>(c->arena_elems, 1)))) return st;
@@ -615,7 +677,6 @@ tn_status build_plan(tn_ctx* c) {
   if ((st = dev_alloc(c, &c->d_one, 1))) return st;
   if ((st = dev_alloc(c, &c->d_partial, (size_t)std::max<int64_t>(partial_elems, 2)))) return st;
   TN_CUDA(cudaMallocHost(&c->h_counter, sizeof(int64_t)));
-  cudaStream_t sm = c->stream;
   if (!tables.empty())
     TN_CUDA(cudaMemcpyAsync(c->d_tables, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice, sm));
   TN_CUDA(cudaMemcpyAsync(c->d_out_pos, c->out_pos.data(), c->out_pos.size() * 4,
@@ -631,7 +692,6 @@ tn_status build_plan(tn_ctx* c) {
   }
   // slice descriptor
   {
-    if (c->sliced.size() > 64) return fail(TN_ERR_DATA, "at most 64 sliced bonds");
     tn::SliceDesc sd{};
     sd.n_sliced = (int32_t)c->sliced.size();
     for (size_t p = 0; p < c->sliced.size(); ++p) sd.dims[p] = c->dim_of[c->sliced[p]];
@@ -654,6 +714,7 @@ tn_status build_plan(tn_ctx* c) {
     sd.absmax_count = n_steps;
     TN_CUDA(cudaMemcpyAsync(c->d_slice_desc, &sd, sizeof(sd), cudaMemcpyHostToDevice, sm));
   }
+  }  // !host_only
   // per-step device descriptors
   std::vector<tn::EinsumDesc> eds(std::max(n_einsum, 1));
   std::vector<tn::PrepDesc> pds(std::max(n_prep, 1));
@@ -812,7 +873,12 @@ tn_status build_plan(tn_ctx* c) {
           const int64_t rs = p.nr ? p.r_s[p.nr - 1] : INT64_MAX;
           const int64_t ks = p.nk ? p.k_s[p.nk - 1] : INT64_MAX;
           p.read_r_fast = rs < ks ? 1 : 0;
-          sp.r_fast[side] = p.read_r_fast;
+        }
+        {
+          const int64_t Kpad_ = sp.Kpad;
+          p.Kpad = Kpad_;
+          p.kind = choose_prep_kind(p, prep_force);
+          sp.r_fast[side] = p.kind;
         }
         int64_t off0 = 0;
         int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
@@ -823,9 +889,19 @@ tn_status build_plan(tn_ctx* c) {
         p.scale_out = c->d_scales + 2 * s + side;
         sp.prep_total[side] = p.plane_elems;
         CUtensorMap* map = side == 0 ? &sp.gemm.mapA : &sp.gemm.mapB;
-        if (!tn::encode_plane_map(map, p.dst, sp.Kpad, sp.R[side], sp.G[side], 4, 128, errbuf,
+        if (!c->host_only &&
+            !tn::encode_plane_map(map, p.dst, sp.Kpad, sp.R[side], sp.G[side], 4, 128, errbuf,
                                   sizeof(errbuf)))
           return fail(TN_ERR_INTERNAL, errbuf);
+        if (c->debug_plan) {
+          fprintf(stderr, "[tn] step %d prep%c G=%lld R=%lld K=%lld kind=%d A=%d B=%d rows:", s,
+                  side ? 'Q' : 'P', (long long)p.G, (long long)p.R, (long long)p.K, p.kind, p.Asz,
+                  p.Bsz);
+          for (int d = 0; d < p.nr; ++d) fprintf(stderr, " %lldx%lld", (long long)p.r_ext[d], (long long)p.r_s[d]);
+          fprintf(stderr, " | k:");
+          for (int d = 0; d < p.nk; ++d) fprintf(stderr, " %lldx%lld", (long long)p.k_ext[d], (long long)p.k_s[d]);
+          fprintf(stderr, "\n");
+        }
       }
       tn::GemmArgs& g = sp.gemm;
       g.J = (int32_t)sp.J;
@@ -847,6 +923,10 @@ tn_status build_plan(tn_ctx* c) {
     }
     live.erase(sp.j);
     live[sp.i] = sp.out;
+  }
+  if (c->host_only) {
+    c->planned = true;
+    return TN_OK;
   }
   if (n_einsum) TN_CUDA(cudaMemcpyAsync(c->d_einsum, eds.data(), n_einsum * sizeof(tn::EinsumDesc),
                                         cudaMemcpyHostToDevice, sm));
@@ -1039,6 +1119,7 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   if (device == -1) {
     tn_ctx* c = new tn_ctx();
     c->host_only = true;
+    c->debug_plan = env_int("TN_DEBUG_PLAN", 0) != 0;
     c->device = -1;
     *out = c;
     return TN_OK;

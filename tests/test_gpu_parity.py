@@ -126,6 +126,12 @@ ROUTES = {
     "tc": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2"},
     "tc_deep": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "100000", "TN_TC_MIN_K": "2",
                 "TN_TC_DEEP_K": "4"},
+    "tc_prep_transpose": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                          "TN_PREP_FORCE": "0"},
+    "tc_prep_direct": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                       "TN_PREP_FORCE": "1"},
+    "tc_prep_general": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8",
+                        "TN_PREP_FORCE": "2"},
     "default": {},
 }
 
@@ -138,7 +144,7 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
     w = configs.small(grid=(3, 4), cycles=8, mode=mode, n_samples=64, n_slices=8, seed=2)
     ref = oracle.contract(w.net, w.path, w.sliced, w.samples)
     out, info = run_gpu(ctx, w)
-    if route in ("tc", "tc_deep"):
+    if route.startswith("tc"):
         assert info["n_tc_steps"] > 0
     if route in ("simt_modes", "simt_wide"):
         c = Contraction(device=-1)
