@@ -201,6 +201,31 @@ __device__ __forceinline__ int64_t decompose(int64_t t, int n, const int64_t* ex
   return off;
 }
 
+// shift-table decomposition (all extents powers of two; sh = log2 extents)
+__device__ __forceinline__ int64_t decompose_sh(int64_t t, int n, const uint8_t* sh,
+                                                const int64_t* stride) {
+  int64_t off = 0;
+  for (int i = n - 1; i >= 0; --i) {
+    const int s = sh[i];
+    off += (t & ((int64_t(1) << s) - 1)) * stride[i];
+    t >>= s;
+  }
+  return off;
+}
+
+__device__ __forceinline__ void store_out_f(const EinsumDesc& d, int64_t idx, float cr, float ci,
+                                            float& amax) {
+  if (d.acc) {
+    double2 o = d.acc[idx];
+    o.x += (double)cr;
+    o.y += (double)ci;
+    d.acc[idx] = o;
+  } else {
+    d.C[idx] = make_float2(cr, ci);
+  }
+  amax = fmaxf(amax, fmaxf(fabsf(cr), fabsf(ci)));
+}
+
 __device__ __forceinline__ void store_out(const EinsumDesc& d, int64_t idx, double cr, double ci,
                                           float& amax) {
   if (d.acc) {
@@ -358,7 +383,7 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
 // smallest-stride free dim v (coalesced reads), the output keeps v innermost
 // (coalesced writes).  These are the HBM-bound "absorb a gate into the stem"
 // steps (stage 1 dominates).  fp32 accumulation (K <= 64 here).
-template <int NMAX>
+template <int NMAX, bool POW2>
 __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __restrict__ gd,
                                                             const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) EinsumDesc d;
@@ -392,7 +417,8 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
       live[u] = m < d.M;
       const int64_t mm = live[u] ? m : m0;
       const int64_t vi = mm % V, o = mm / V;
-      a_row[u] = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
+      a_row[u] = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
+                           : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
       obase[u] = o * N * V + vi;
     }
     float accr[U][NMAX], acci[U][NMAX];
@@ -423,7 +449,7 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
       if (live[u])
 #pragma unroll
         for (int n = 0; n < NMAX; ++n)
-          if (n < N) store_out(d, obase[u] + (int64_t)n * V, accr[u][n], acci[u][n], amax);
+          if (n < N) store_out_f(d, obase[u] + (int64_t)n * V, accr[u][n], acci[u][n], amax);
   }
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
@@ -592,11 +618,16 @@ cudaError_t enable_einsum_smem() {
   static bool done = false;
   if (done) return cudaSuccess;
   cudaError_t e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<4>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<8>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<16>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<32>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<64>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<4, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<8, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<16, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<32, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<64, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<4, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<8, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<16, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<32, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny_kernel<64, false>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_wide_kernel<2>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_wide_kernel<4>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_wide_kernel<8>)) != cudaSuccess) return e;
@@ -615,11 +646,15 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
   if (h.mode == 1) {
     const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
     const int g = grid_for(h.M, th);
-    if (h.N <= 4) einsum_skinny_kernel<4><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else if (h.N <= 8) einsum_skinny_kernel<8><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else if (h.N <= 16) einsum_skinny_kernel<16><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else if (h.N <= 32) einsum_skinny_kernel<32><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else einsum_skinny_kernel<64><<<g, th, smem, s>>>(d_desc, leaf_off);
+#define TN_SKINNY(NM)                                                                     \
+  (h.pow2 ? einsum_skinny_kernel<NM, true><<<g, th, smem, s>>>(d_desc, leaf_off)          \
+          : einsum_skinny_kernel<NM, false><<<g, th, smem, s>>>(d_desc, leaf_off))
+    if (h.N <= 4) TN_SKINNY(4);
+    else if (h.N <= 8) TN_SKINNY(8);
+    else if (h.N <= 16) TN_SKINNY(16);
+    else if (h.N <= 32) TN_SKINNY(32);
+    else TN_SKINNY(64);
+#undef TN_SKINNY
     return cudaGetLastError();
   }
   if (h.mode == 3) {

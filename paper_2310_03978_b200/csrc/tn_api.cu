@@ -322,6 +322,17 @@ int choose_prep_kind(tn::PrepDesc& p, int force) {
   return 2;
 }
 
+// log2 shift tables for the SIMT kernels (pow2 = every extent a power of two)
+void fill_shifts(tn::EinsumDesc& e) {
+  auto lg = [](int64_t x) -> int { int s = 0; while ((int64_t(1) << s) < x) ++s; return s; };
+  auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+  bool ok = true;
+  for (int i = 0; i < e.nm; ++i) { ok &= p2(e.m_ext[i]); e.m_sh[i] = (uint8_t)lg(e.m_ext[i]); }
+  for (int i = 0; i < e.nn; ++i) { ok &= p2(e.n_ext[i]); e.n_sh[i] = (uint8_t)lg(e.n_ext[i]); }
+  for (int i = 0; i < e.nk; ++i) { ok &= p2(e.k_ext[i]); e.k_sh[i] = (uint8_t)lg(e.k_ext[i]); }
+  e.pow2 = ok ? 1 : 0;
+}
+
 void contiguous_strides(std::vector<VDim>& d) {
   int64_t s = 1;
   for (int p = (int)d.size() - 1; p >= 0; --p) {
@@ -821,6 +832,7 @@ tn_status build_plan(tn_ctx* c) {
       for (int p = 0; p < e.nk; ++p) { e.k_ext[p] = Kx[p].ext; e.k_sa[p] = Kx[p].sa; e.k_sb[p] = Kx[p].sb; }
       e.absmax_out = absmax_out;
       e.acc = sp.final_step ? c->d_acc : nullptr;
+      fill_shifts(e);
       sp.hdesc = e;
     } else if (!sp.tc) {
       tn::EinsumDesc& e = eds[sp.einsum_idx];
@@ -845,6 +857,7 @@ tn_status build_plan(tn_ctx* c) {
         e.partial = c->d_partial;
         e.kchunk = 1 << 16;
       }
+      fill_shifts(e);
       sp.hdesc = e;
     } else {
       // P operand = A side unless swapped; both share the canonical K order
@@ -1136,7 +1149,7 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   c->num_sms = prop.multiProcessorCount;
   c->kchunk3 = env_int("TN_KCHUNK3", 1);
-  c->kchunk1 = env_int("TN_KCHUNK1", 0);
+  c->kchunk1 = env_int("TN_KCHUNK1", 4);   // 1-pass: promote every 4 k-blocks (128 k)
   c->group_m = env_int("TN_GEMM_GROUP", 8);   // best of {1,8,16,32} on 8192^2 x 16384
   *out = c;
   return TN_OK;
@@ -1452,6 +1465,7 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     e.nm = 1; e.m_ext[0] = m; e.m_sa[0] = k;
     e.nn = 1; e.n_ext[0] = n; e.n_sb[0] = k;
     e.nk = 1; e.k_ext[0] = k; e.k_sa[0] = 1; e.k_sb[0] = 1;
+    fill_shifts(e);
     tn::EinsumDesc* d = nullptr;
     TN_CUDA(cudaMalloc(&d, sizeof(e)));
     TN_CUDA(cudaMemcpyAsync(d, &e, sizeof(e), cudaMemcpyHostToDevice, sm));

@@ -30,7 +30,8 @@ struct EinsumDesc {
   // mode: 0 general (one thread per output), 1 skinny (B = small operand staged in
   // smem, output layout [Mo][N][V] with V = A's smallest-stride free dim, which is
   // m_ext/m_sa[nm-1] here), 2 split-K dot (few outputs, long K; fp64 partials)
-  int32_t mode, pad_;
+  int32_t mode, pow2;             // pow2: every m/n/k extent is a power of two (shift tables valid)
+  uint8_t m_sh[TN_MAXD], n_sh[TN_MAXD], k_sh[TN_MAXD];   // log2 of the extents
   int64_t V;                      // mode 1: extent of the vector (lane) dim
   double* partial;                // mode 2: fp64 partial sums [2*J*M*N] (zeroed per launch)
   int64_t kchunk;                 // mode 2: k elements per block

@@ -35,7 +35,7 @@ def main(out):
     steps = ctx.plan_json()["steps"]
     tc = sorted([s["tcc"] for s in steps if s["route"] == "tcgen05"], reverse=True)
     total = sum(s["tcc"] for s in steps)
-    ks = [0, 1, 10, 50, len(tc)]
+    ks = sorted({k for k in (0, 1, 10, 50, len(tc)) if k <= len(tc)})
     res = []
     for k in ks:
         prec = "extended" if k == 0 else "mixed"
