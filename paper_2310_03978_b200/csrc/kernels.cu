@@ -309,17 +309,23 @@ __global__ void __launch_bounds__(256, 4) prep_gt_kernel(const PrepDesc* __restr
     dstB[b] = decompose(b, d.nb, d.b_ext, d.b_dst);
   }
   const int64_t plane = d.plane_elems;
+  __shared__ int64_t tile_off[2];
+  const int as_sh = __ffs(As) - 1, hb_sh = __ffs(Bs / 2) - 1;   // block sizes are powers of two
   for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
-    const int64_t sc = decompose(c, d.nc, d.c_ext, d.c_src);
-    const int64_t dc = decompose(c, d.nc, d.c_ext, d.c_dst);
     __syncthreads();   // offset tables ready / previous tile consumed
+    if (threadIdx.x == 0) {
+      tile_off[0] = decompose(c, d.nc, d.c_ext, d.c_src);
+      tile_off[1] = decompose(c, d.nc, d.c_ext, d.c_dst);
+    }
+    __syncthreads();
+    const int64_t sc = tile_off[0], dc = tile_off[1];
     for (int e = threadIdx.x; e < As * Bs; e += blockDim.x) {
-      const int a = e % As, b = e / As;
+      const int a = e & (As - 1), b = e >> as_sh;
       tile[b][a] = src[sc + srcA[a] + srcB[b]];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < As * Bs / 2; e += blockDim.x) {
-      const int b = (e % (Bs / 2)) * 2, a = e / (Bs / 2);
+      const int b = (e & (Bs / 2 - 1)) * 2, a = e >> hb_sh;
       const float2 v0 = tile[b][a], v1 = tile[b + 1][a];
       const float xr0 = v0.x * scale, xi0 = v0.y * scale, xr1 = v1.x * scale, xi1 = v1.y * scale;
       const __half2 hr = __floats2half2_rn(xr0, xr1), hi = __floats2half2_rn(xi0, xi1);
