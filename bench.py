@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c3", "c2"])
     ap.add_argument("--boundary", default="single")
     ap.add_argument("--peak", type=int, default=32)
     ap.add_argument("--order-tag", default="a64", help="order file variant (tools/make_orders.py)")
@@ -57,6 +57,8 @@ def load_workload(args):
     from tnworkloads import configs
     if args.workload == "c2":
         return configs.c2()
+    if args.workload == "c3":
+        return configs.c3()
     return configs.c4(args.boundary, args.peak, args.order_tag)
 
 

@@ -291,45 +291,56 @@ __global__ void __launch_bounds__(256, 4) prep_direct_kernel(const PrepDesc* __r
 // offset tables live in smem, so reads walk the source's innermost run and the
 // half2 plane stores walk the destination's, whatever the interleaving.
 template <int PLANES>
-__global__ void __launch_bounds__(256, 4) prep_gt_kernel(const PrepDesc* __restrict__ gd,
+__global__ void __launch_bounds__(256, 3) prep_gt_kernel(const PrepDesc* __restrict__ gd,
                                                          const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) PrepDesc d;
   copy_desc_to_smem(&d, gd);
-  __shared__ int64_t srcA[64], dstA[64], srcB[64], dstB[64];
-  __shared__ float2 tile[64][33];                     // [b][a], a <= 32
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int T = d.T;
+  int64_t* srcoff = reinterpret_cast<int64_t*>(dyn);            // [T] source order
+  int64_t* dstoff = srcoff + T;                                  // [T] destination order
+  float2* tile = reinterpret_cast<float2*>(dstoff + T);          // [T] source order
+  int32_t* spos = reinterpret_cast<int32_t*>(tile + T);          // [T] dst order -> src index
   const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
   const float scale = prep_scale(d);
-  const int As = d.Asz, Bs = d.Bsz;
-  if (threadIdx.x < As) {
-    srcA[threadIdx.x] = decompose(threadIdx.x, d.na, d.a_ext, d.a_src);
-    dstA[threadIdx.x] = decompose(threadIdx.x, d.na, d.a_ext, d.a_dst);
-  } else if (threadIdx.x >= 64 && threadIdx.x - 64 < Bs) {
-    const int b = threadIdx.x - 64;
-    srcB[b] = decompose(b, d.nb, d.b_ext, d.b_src);
-    dstB[b] = decompose(b, d.nb, d.b_ext, d.b_dst);
+  // tile tables, once per block
+  for (int e = threadIdx.x; e < T; e += blockDim.x) {
+    int64_t t = e, so = 0;
+    for (int i = d.nt - 1; i >= 0; --i) {        // source-order digits
+      so += (t % d.ts_ext[i]) * d.ts_src[i];
+      t /= d.ts_ext[i];
+    }
+    srcoff[e] = so;
+    int64_t f = e, pos = 0, dof = 0;
+    for (int i = d.nt - 1; i >= 0; --i) {        // destination-order digits of element f = e
+      const int p = d.td_pos[i];
+      const int64_t digit = f % d.td_ext[i];
+      f /= d.td_ext[i];
+      int64_t lstride = 1;
+      for (int q = p + 1; q < d.nt; ++q) lstride *= d.ts_ext[q];
+      pos += digit * lstride;
+      dof += digit * d.ts_dst[p];
+    }
+    spos[e] = (int32_t)pos;
+    dstoff[e] = dof;
   }
   const int64_t plane = d.plane_elems;
   __shared__ int64_t tile_off[2];
-  const int as_sh = __ffs(As) - 1, hb_sh = __ffs(Bs / 2) - 1;   // block sizes are powers of two
   for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
-    __syncthreads();   // offset tables ready / previous tile consumed
+    __syncthreads();   // tables ready / previous tile consumed
     if (threadIdx.x == 0) {
       tile_off[0] = decompose(c, d.nc, d.c_ext, d.c_src);
       tile_off[1] = decompose(c, d.nc, d.c_ext, d.c_dst);
     }
     __syncthreads();
     const int64_t sc = tile_off[0], dc = tile_off[1];
-    for (int e = threadIdx.x; e < As * Bs; e += blockDim.x) {
-      const int a = e & (As - 1), b = e >> as_sh;
-      tile[b][a] = src[sc + srcA[a] + srcB[b]];
-    }
+    for (int e = threadIdx.x; e < T; e += blockDim.x) tile[e] = src[sc + srcoff[e]];
     __syncthreads();
-    for (int e = threadIdx.x; e < As * Bs / 2; e += blockDim.x) {
-      const int b = (e & (Bs / 2 - 1)) * 2, a = e >> hb_sh;
-      const float2 v0 = tile[b][a], v1 = tile[b + 1][a];
+    for (int f = 2 * threadIdx.x; f < T; f += 2 * blockDim.x) {
+      const float2 v0 = tile[spos[f]], v1 = tile[spos[f + 1]];
       const float xr0 = v0.x * scale, xi0 = v0.y * scale, xr1 = v1.x * scale, xi1 = v1.y * scale;
       const __half2 hr = __floats2half2_rn(xr0, xr1), hi = __floats2half2_rn(xi0, xi1);
-      const int64_t idx = dc + dstA[a] + dstB[b];     // dstB[b+1] = dstB[b] + 1, idx even
+      const int64_t idx = dc + dstoff[f];             // dstoff[f+1] = dstoff[f] + 1, idx even
       reinterpret_cast<__half2*>(d.dst + idx)[0] = hr;
       reinterpret_cast<__half2*>(d.dst + plane + idx)[0] = hi;
       if (PLANES == 4) {
@@ -586,16 +597,23 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind,
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
                         const int64_t* leaf_off, cudaStream_t s) {
   const int th = 256;
-  if (kind == 2) {   // general transposer, 2048-element tiles
-    int64_t tiles = total / 2048;
-    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 8);
+  if (kind == 2) {   // general transposer, tiles of T <= 4096 elements
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(prep_gt_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+      cudaFuncSetAttribute(prep_gt_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+      attr = true;
+    }
+    const size_t smem = (size_t)tile_T * (8 + 8 + 8 + 4);
+    int64_t tiles = total / std::max(tile_T, 1);
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 6);
     if (planes == 4)
-      prep_gt_kernel<4><<<g, th, 0, s>>>(d_desc, leaf_off);
+      prep_gt_kernel<4><<<g, th, smem, s>>>(d_desc, leaf_off);
     else
-      prep_gt_kernel<2><<<g, th, 0, s>>>(d_desc, leaf_off);
+      prep_gt_kernel<2><<<g, th, smem, s>>>(d_desc, leaf_off);
     return cudaGetLastError();
   }
   if (kind == 1) {   // k-walking source: direct kernel, 8 elements per thread

@@ -74,6 +74,7 @@ struct StepPlan {
   int64_t R[2] = {0, 0}, Kpad = 0, G[2] = {1, 1};
   int in_slot[2] = {0, 0};
   int r_fast[2] = {0, 0};       // prep kernel kind per side (choose_prep_kind)
+  int gtT[2] = {0, 0};          // general-transposer tile size per side
   int mode = 0;                 // SIMT mode: 0 general, 1 skinny, 2 split-K dot
   bool x_is_b = false;          // skinny: the big (streamed) operand is B
   std::vector<int64_t> vlabels; // skinny: labels of the lane (vector) run, outer -> inner
@@ -276,49 +277,78 @@ int choose_prep_kind(tn::PrepDesc& p, int force) {
   for (int d = p.nr - 1; d >= 0; --d) { pool.push_back({p.r_ext[d], p.r_s[d], t}); t *= p.r_ext[d]; }
   t = 1;
   for (int d = p.nk - 1; d >= 0; --d) { pool.push_back({p.k_ext[d], p.k_s[d], t}); t *= p.k_ext[d]; }
-  // take a block of `target` elements from the pool, walking `key` (dst or src
-  // stride) upward; the last dim is split when it overshoots (power-of-two dims)
-  auto take = [&](int64_t target, bool by_dst, std::vector<D>& blk) -> int64_t {
-    int64_t size = 1;
-    while (size < target && !pool.empty()) {
-      int best = 0;
-      for (int q = 1; q < (int)pool.size(); ++q)
-        if ((by_dst ? pool[q].t : pool[q].s) < (by_dst ? pool[best].t : pool[best].s)) best = q;
-      D x = pool[best];
-      if (by_dst && x.t != size) break;             // destination block must stay contiguous
-      const int64_t need = (target + size - 1) / size;
-      if (x.e > need && x.e % need == 0) {
-        blk.push_back({need, x.s, x.t});
-        pool[best] = {x.e / need, x.s * need, x.t * need};
-        size *= need;
-      } else {
-        blk.push_back(x);
-        pool.erase(pool.begin() + best);
-        size *= x.e;
-      }
+  // Tile = set of dims holding the source's innermost run (>= 32 elements, walked
+  // by the load phase) and the destination's contiguous k-run (>= 64, walked by
+  // the half2 store phase).  Dims are split (power-of-two extents) to hit sizes.
+  std::vector<D> tl;
+  auto grab = [&](int q, int64_t need) {          // move (the inner `need` part of) pool[q]
+    D x = pool[q];
+    if (x.e > need && x.e % need == 0) {
+      tl.push_back({need, x.s, x.t});
+      pool[q] = {x.e / need, x.s * need, x.t * need};
+    } else {
+      tl.push_back(x);
+      pool.erase(pool.begin() + q);
     }
-    return size;
   };
-  std::vector<D> B, A;
-  const int64_t bs = take(64, true, B);
-  const int64_t as = take(32, false, A);
-  if (bs % 2 != 0 || bs > 64 || as > 32 || (int)B.size() > 8 || (int)A.size() > 8 ||
-      (int)pool.size() > TN_MAXD || (bs & (bs - 1)) || (as & (as - 1)))   // kernel uses shifts
+  int64_t run = 1;                                 // source run
+  while (run < 32 && !pool.empty()) {
+    int q = 0;
+    for (int i = 1; i < (int)pool.size(); ++i) if (pool[i].s < pool[q].s) q = i;
+    const int64_t before = tl.size();
+    grab(q, (32 + run - 1) / run);
+    run *= tl[before].e;
+  }
+  int64_t drun = 1;                                // destination run (stride-1 chain)
+  while (drun < 64) {
+    int q = -1;
+    bool in_tile = false;
+    for (int i = 0; i < (int)tl.size(); ++i) if (tl[i].t == drun) { q = i; in_tile = true; }
+    if (!in_tile)
+      for (int i = 0; i < (int)pool.size(); ++i) if (pool[i].t == drun) q = i;
+    if (q < 0) break;
+    if (in_tile) {
+      drun *= tl[q].e;
+    } else {
+      const int64_t before = tl.size();
+      grab(q, (64 + drun - 1) / drun);
+      drun *= tl[before].e;
+    }
+  }
+  int64_t T = 1;
+  for (auto& x : tl) T *= x.e;
+  while (T < 1024 && !pool.empty()) {             // amortise the per-tile overhead
+    int q = 0;
+    for (int i = 1; i < (int)pool.size(); ++i) if (pool[i].s < pool[q].s) q = i;
+    const int64_t before = tl.size();
+    grab(q, (1024 + T - 1) / T);
+    T *= tl[before].e;
+  }
+  if (drun < 2 || drun % 2 != 0 || T > 4096 || T % 2 != 0 || (int)tl.size() > 12 ||
+      (int)pool.size() > TN_MAXD)
     return p.read_r_fast ? 0 : 1;
-  // block index order: row-major over the listed dims, so list them outer -> inner
-  std::reverse(B.begin(), B.end());
-  std::reverse(A.begin(), A.end());
-  p.nb = (int)B.size();
-  for (int i = 0; i < p.nb; ++i) { p.b_ext[i] = B[i].e; p.b_src[i] = B[i].s; p.b_dst[i] = B[i].t; }
-  p.na = (int)A.size();
-  for (int i = 0; i < p.na; ++i) { p.a_ext[i] = A[i].e; p.a_src[i] = A[i].s; p.a_dst[i] = A[i].t; }
+  // source order (outer -> inner = descending source stride) and destination order
+  std::vector<D> ts = tl, td = tl;
+  std::sort(ts.begin(), ts.end(), [](const D& a, const D& b) { return a.s > b.s; });
+  std::vector<int> idx(tl.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return tl[a].t > tl[b].t; });
+  p.nt = (int)tl.size();
+  for (int i = 0; i < p.nt; ++i) { p.ts_ext[i] = ts[i].e; p.ts_src[i] = ts[i].s; p.ts_dst[i] = ts[i].t; }
+  for (int i = 0; i < p.nt; ++i) {
+    const D& x = tl[idx[i]];
+    p.td_ext[i] = x.e;
+    int pos = -1;
+    for (int j = 0; j < p.nt; ++j)
+      if (ts[j].s == x.s && ts[j].t == x.t && ts[j].e == x.e) pos = j;
+    p.td_pos[i] = pos;
+  }
   p.nc = (int)pool.size();
   p.nC = 1;
   for (int i = 0; i < p.nc; ++i) {
     p.c_ext[i] = pool[i].e; p.c_src[i] = pool[i].s; p.c_dst[i] = pool[i].t; p.nC *= pool[i].e;
   }
-  p.Asz = (int32_t)as;
-  p.Bsz = (int32_t)bs;
+  p.T = (int32_t)T;
   return 2;
 }
 
@@ -892,6 +922,7 @@ tn_status build_plan(tn_ctx* c) {
           p.Kpad = Kpad_;
           p.kind = choose_prep_kind(p, prep_force);
           sp.r_fast[side] = p.kind;
+          sp.gtT[side] = p.kind == 2 ? p.T : 0;
         }
         int64_t off0 = 0;
         int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
@@ -907,9 +938,8 @@ tn_status build_plan(tn_ctx* c) {
                                   sizeof(errbuf)))
           return fail(TN_ERR_INTERNAL, errbuf);
         if (c->debug_plan) {
-          fprintf(stderr, "[tn] step %d prep%c G=%lld R=%lld K=%lld kind=%d A=%d B=%d rows:", s,
-                  side ? 'Q' : 'P', (long long)p.G, (long long)p.R, (long long)p.K, p.kind, p.Asz,
-                  p.Bsz);
+          fprintf(stderr, "[tn] step %d prep%c G=%lld R=%lld K=%lld kind=%d T=%d rows:", s,
+                  side ? 'Q' : 'P', (long long)p.G, (long long)p.R, (long long)p.K, p.kind, p.T);
           for (int d = 0; d < p.nr; ++d) fprintf(stderr, " %lldx%lld", (long long)p.r_ext[d], (long long)p.r_s[d]);
           fprintf(stderr, " | k:");
           for (int d = 0; d < p.nk; ++d) fprintf(stderr, " %lldx%lld", (long long)p.k_ext[d], (long long)p.k_s[d]);
@@ -1002,7 +1032,7 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
         for (int side = 0; side < 2; ++side) {
           Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes));
           TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
-                                  sp.r_fast[side], c->d_leaf_off, sm));
+                                  sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm));
         }
         tn::GemmArgs ga = sp.gemm;
         ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
@@ -1507,8 +1537,8 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     TN_CUDA(cudaMalloc(&dp, sizeof(p)));
     TN_CUDA(cudaMemcpyAsync(dp, p, sizeof(p), cudaMemcpyHostToDevice, sm));
     const int planes = passes == 3 ? 4 : 2;
-    TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, 0, nullptr, sm));
-    TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, 0, nullptr, sm));
+    TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, 0, 0, nullptr, sm));
+    TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, 0, 0, nullptr, sm));
     g.J = (int32_t)J; g.M = (int32_t)m; g.N = (int32_t)n; g.K = (int32_t)k;
     g.ia = ia; g.ib = ib;
     g.C = reinterpret_cast<float2*>(C);

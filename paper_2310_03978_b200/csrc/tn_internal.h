@@ -48,15 +48,17 @@ struct PrepDesc {
   int64_t r_ext[TN_MAXD], r_s[TN_MAXD];
   int64_t k_ext[TN_MAXD], k_s[TN_MAXD];
   int32_t read_r_fast, pad_;      // 1: source stride of rows < of k (read along r)
-  // general transposer (kind 2): logical index = (c outer, b dst-inner, a src-inner);
-  // element (c,b,a) reads src[c_src + b_src + a_src] and writes plane offset
-  // c_dst + b_dst + a_dst; block B is the destination's contiguous run (stride 1)
+  // general transposer (kind 2): the tile is the product of the dims t_* (which hold
+  // both the source's and the destination's innermost contiguous runs); outer dims
+  // c_*.  t dims are listed twice: in source-stride order (ts_*) and in destination-
+  // stride order (td_*), with td_pos[i] = position of td dim i in the ts list.
   int32_t kind;                   // 0 transposer(r/k), 1 direct, 2 general transposer
-  int32_t na, nb, nc;
-  int32_t Asz, Bsz;
+  int32_t nt, nc;
+  int32_t T, pad2_;
   int64_t nC;
-  int64_t a_ext[8], a_src[8], a_dst[8];
-  int64_t b_ext[8], b_src[8], b_dst[8];
+  int64_t ts_ext[12], ts_src[12], ts_dst[12];   // source order, outer -> inner
+  int64_t td_ext[12];
+  int32_t td_pos[12];                           // destination order, outer -> inner
   int64_t c_ext[TN_MAXD], c_src[TN_MAXD], c_dst[TN_MAXD];
   __half* dst; int64_t plane_elems;
   const unsigned* absmax_in;      // absmax of the source tensor (float bits)
@@ -94,7 +96,7 @@ struct SliceDesc {
 
 // kernel launchers (kernels.cu / gemm_tcgen05.cu)
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
-cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind,
+cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
                         const int64_t* leaf_off, cudaStream_t s);
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
                           const int64_t* leaf_off, cudaStream_t s);
