@@ -303,26 +303,12 @@ __global__ void __launch_bounds__(256, 3) prep_gt_kernel(const PrepDesc* __restr
   int32_t* spos = reinterpret_cast<int32_t*>(tile + T);          // [T] dst order -> src index
   const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
   const float scale = prep_scale(d);
-  // tile tables, once per block
+  // tile tables (computed once at plan time), copied into smem
+  const int32_t* gspos = reinterpret_cast<const int32_t*>(d.gt_tab + 2 * T);
   for (int e = threadIdx.x; e < T; e += blockDim.x) {
-    int64_t t = e, so = 0;
-    for (int i = d.nt - 1; i >= 0; --i) {        // source-order digits
-      so += (t % d.ts_ext[i]) * d.ts_src[i];
-      t /= d.ts_ext[i];
-    }
-    srcoff[e] = so;
-    int64_t f = e, pos = 0, dof = 0;
-    for (int i = d.nt - 1; i >= 0; --i) {        // destination-order digits of element f = e
-      const int p = d.td_pos[i];
-      const int64_t digit = f % d.td_ext[i];
-      f /= d.td_ext[i];
-      int64_t lstride = 1;
-      for (int q = p + 1; q < d.nt; ++q) lstride *= d.ts_ext[q];
-      pos += digit * lstride;
-      dof += digit * d.ts_dst[p];
-    }
-    spos[e] = (int32_t)pos;
-    dstoff[e] = dof;
+    srcoff[e] = d.gt_tab[e];
+    dstoff[e] = d.gt_tab[T + e];
+    spos[e] = gspos[e];
   }
   const int64_t plane = d.plane_elems;
   __shared__ int64_t tile_off[2];
@@ -467,6 +453,67 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
 #pragma unroll
         for (int n = 0; n < NMAX; ++n)
           if (n < N) store_out_f(d, obase[u] + (int64_t)n * V, accr[u][n], acci[u][n], amax);
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+// Vectorised variant: the lane run v is unit-stride and even, so a thread owns the
+// pair (v, v+1): one 16-byte load per k and one 16-byte store per n (pairs are
+// adjacent in A and in C), half the instructions per byte of the scalar kernel.
+template <int NMAX, bool POW2>
+__global__ void __launch_bounds__(256) einsum_skinny2_kernel(const EinsumDesc* __restrict__ gd,
+                                                             const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int K = (int)d.K, N = (int)d.N;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][N]
+  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * N);
+  const float2* A = d.A + d.a_off;
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int k = e / N, n = e % N;
+    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
+  __syncthreads();
+  const int64_t V = d.V, Vh = V / 2, Mh = d.M / 2;
+  float amax = 0.f;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mh;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t vi = (m % Vh) * 2, o = m / Vh;
+    const float2* a_row = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
+                                    : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi;
+    float r0[NMAX], i0[NMAX], r1[NMAX], i1[NMAX];
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) { r0[n] = 0.f; i0[n] = 0.f; r1[n] = 0.f; i1[n] = 0.f; }
+    for (int k = 0; k < K; ++k) {
+      const float4 q = *reinterpret_cast<const float4*>(a_row + koff[k]);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n < N) {
+          const float2 b = Bs[k * N + n];
+          r0[n] = fmaf(q.x, b.x, r0[n]); r0[n] = fmaf(-q.y, b.y, r0[n]);
+          i0[n] = fmaf(q.x, b.y, i0[n]); i0[n] = fmaf(q.y, b.x, i0[n]);
+          r1[n] = fmaf(q.z, b.x, r1[n]); r1[n] = fmaf(-q.w, b.y, r1[n]);
+          i1[n] = fmaf(q.z, b.y, i1[n]); i1[n] = fmaf(q.w, b.x, i1[n]);
+        }
+      }
+    }
+    const int64_t base = o * N * V + vi;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n < N) {
+        const int64_t idx = base + (int64_t)n * V;
+        if (d.acc) {
+          store_out_f(d, idx, r0[n], i0[n], amax);
+          store_out_f(d, idx + 1, r1[n], i1[n], amax);
+        } else {
+          *reinterpret_cast<float4*>(d.C + idx) = make_float4(r0[n], i0[n], r1[n], i1[n]);
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0[n]), fabsf(i0[n])), fmaxf(fabsf(r1[n]), fabsf(i1[n]))));
+        }
+      }
+    }
   }
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
@@ -631,6 +678,15 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
   return cudaGetLastError();
 }
 
+bool tn_vec2_enabled() {   // TN_SKINNY_VEC2=0 disables the paired-lane kernel (tests)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TN_SKINNY_VEC2");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 template <typename F>
 cudaError_t allow_big_smem(F* kern) {
   // the staged small operand can exceed the 48 KB default dynamic smem window
@@ -652,6 +708,12 @@ cudaError_t enable_einsum_smem() {
   if ((e = allow_big_smem(einsum_skinny_kernel<16, false>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_skinny_kernel<32, false>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_skinny_kernel<64, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny2_kernel<4, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny2_kernel<8, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny2_kernel<16, true>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny2_kernel<4, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny2_kernel<8, false>)) != cudaSuccess) return e;
+  if ((e = allow_big_smem(einsum_skinny2_kernel<16, false>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_wide_kernel<2>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_wide_kernel<4>)) != cudaSuccess) return e;
   if ((e = allow_big_smem(einsum_wide_kernel<8>)) != cudaSuccess) return e;
@@ -670,9 +732,15 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
   if (h.mode == 1) {
     const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
     const int g = grid_for(h.M, th);
+    // pairs of lanes (16-B accesses) when the lane run is unit-stride, even and the
+    // big operand is an aligned intermediate (never a leaf with a slice offset)
+    const bool vec2 = h.pow2 && h.m_sa[h.nm - 1] == 1 && h.V % 2 == 0 && h.a_leaf < 0 &&
+                      h.a_off % 2 == 0 && h.N <= 16 && tn_vec2_enabled();
 #define TN_SKINNY(NM)                                                                     \
-  (h.pow2 ? einsum_skinny_kernel<NM, true><<<g, th, smem, s>>>(d_desc, leaf_off)          \
-          : einsum_skinny_kernel<NM, false><<<g, th, smem, s>>>(d_desc, leaf_off))
+  (vec2 ? (h.pow2 ? einsum_skinny2_kernel<NM, true><<<grid_for(h.M / 2, th), th, smem, s>>>(d_desc, leaf_off) \
+                  : einsum_skinny2_kernel<NM, false><<<grid_for(h.M / 2, th), th, smem, s>>>(d_desc, leaf_off)) \
+        : (h.pow2 ? einsum_skinny_kernel<NM, true><<<g, th, smem, s>>>(d_desc, leaf_off)  \
+                  : einsum_skinny_kernel<NM, false><<<g, th, smem, s>>>(d_desc, leaf_off)))
     if (h.N <= 4) TN_SKINNY(4);
     else if (h.N <= 8) TN_SKINNY(8);
     else if (h.N <= 16) TN_SKINNY(16);

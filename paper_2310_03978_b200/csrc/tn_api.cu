@@ -157,6 +157,7 @@ struct tn_ctx {
   tn::PrepDesc* d_prep = nullptr;
   float2* d_one = nullptr;
   double* d_partial = nullptr;     // split-K dot partial sums
+  int64_t* d_gt = nullptr;         // general-transposer tile tables
   int64_t device_bytes = 0;
   // profiling
   bool profiling = false;
@@ -193,7 +194,7 @@ void free_dev(tn_ctx* c) {
   if (c->host_only) { c->planned = false; return; }
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
-                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial};
+                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_counter) cudaFreeHost(c->h_counter);
@@ -202,6 +203,7 @@ void free_dev(tn_ctx* c) {
   c->d_out_pos = nullptr; c->d_slice_desc = nullptr; c->d_terms_i = nullptr; c->d_terms_s = nullptr;
   c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr; c->h_counter = nullptr;
   c->d_partial = nullptr;
+  c->d_gt = nullptr;
   c->planned = false;
 }
 
@@ -350,6 +352,33 @@ int choose_prep_kind(tn::PrepDesc& p, int force) {
   }
   p.T = (int32_t)T;
   return 2;
+}
+
+// General-transposer tile tables (plan time): srcoff[e] for tile element e in
+// source order, then dstoff[f] and the source-order position spos[f] of element f
+// in destination order (int32, packed two per int64 word).
+std::vector<int64_t> gt_tables(const tn::PrepDesc& p) {
+  const int T = p.T, nt = p.nt;
+  std::vector<int64_t> tab(2 * (size_t)T + ((size_t)T + 1) / 2, 0);
+  int32_t* spos = reinterpret_cast<int32_t*>(tab.data() + 2 * T);
+  std::vector<int64_t> lstride(nt, 1);
+  for (int q = nt - 2; q >= 0; --q) lstride[q] = lstride[q + 1] * p.ts_ext[q + 1];
+  for (int e = 0; e < T; ++e) {
+    int64_t t = e, so = 0;
+    for (int i = nt - 1; i >= 0; --i) { so += (t % p.ts_ext[i]) * p.ts_src[i]; t /= p.ts_ext[i]; }
+    tab[e] = so;
+    int64_t f = e, pos = 0, dof = 0;
+    for (int i = nt - 1; i >= 0; --i) {
+      const int q = p.td_pos[i];
+      const int64_t digit = f % p.td_ext[i];
+      f /= p.td_ext[i];
+      pos += digit * lstride[q];
+      dof += digit * p.ts_dst[q];
+    }
+    tab[T + e] = dof;
+    spos[e] = (int32_t)pos;
+  }
+  return tab;
 }
 
 // log2 shift tables for the SIMT kernels (pow2 = every extent a power of two)
@@ -759,6 +788,8 @@ tn_status build_plan(tn_ctx* c) {
   // per-step device descriptors
   std::vector<tn::EinsumDesc> eds(std::max(n_einsum, 1));
   std::vector<tn::PrepDesc> pds(std::max(n_prep, 1));
+  std::vector<int64_t> gt_all;             // concatenated GT tables
+  std::vector<std::pair<int, int64_t>> gt_ref;   // (prep index, offset in gt_all)
   auto base_of = [&](const View& v) -> const float2* { return v.buf == 0 ? c->d_leaf : c->d_arena; };
   // rebuild the live views to fill descriptors (same replay as above)
   live.clear();
@@ -923,6 +954,11 @@ tn_status build_plan(tn_ctx* c) {
           p.kind = choose_prep_kind(p, prep_force);
           sp.r_fast[side] = p.kind;
           sp.gtT[side] = p.kind == 2 ? p.T : 0;
+          if (p.kind == 2) {
+            std::vector<int64_t> tab = gt_tables(p);
+            gt_ref.push_back({sp.prep_idx + side, (int64_t)gt_all.size()});
+            gt_all.insert(gt_all.end(), tab.begin(), tab.end());
+          }
         }
         int64_t off0 = 0;
         int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
@@ -973,6 +1009,12 @@ tn_status build_plan(tn_ctx* c) {
   }
   if (n_einsum) TN_CUDA(cudaMemcpyAsync(c->d_einsum, eds.data(), n_einsum * sizeof(tn::EinsumDesc),
                                         cudaMemcpyHostToDevice, sm));
+  if (!gt_all.empty()) {
+    tn_status st2 = dev_alloc(c, &c->d_gt, gt_all.size());
+    if (st2) return st2;
+    TN_CUDA(cudaMemcpyAsync(c->d_gt, gt_all.data(), gt_all.size() * 8, cudaMemcpyHostToDevice, sm));
+    for (auto& r : gt_ref) pds[r.first].gt_tab = c->d_gt + r.second;
+  }
   if (n_prep) TN_CUDA(cudaMemcpyAsync(c->d_prep, pds.data(), n_prep * sizeof(tn::PrepDesc),
                                       cudaMemcpyHostToDevice, sm));
   TN_CUDA(cudaStreamSynchronize(sm));
