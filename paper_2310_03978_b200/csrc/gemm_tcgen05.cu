@@ -47,8 +47,6 @@ namespace {
 
 constexpr int BM = 128, BN = 128, BK = 32;          // BK in complex k (64 B fp16 rows)
 constexpr int PLANE_TILE = 128 * BK * 2;            // 8 KiB per plane tile
-constexpr int NUM_EPI_WARPS = 8;
-constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr uint32_t TMEM_COLS = 512;
 
 template <int PASSES>
@@ -161,8 +159,8 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int64_t tile, int
   }
 }
 
-template <int PASSES>
-__global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
+template <int PASSES, int EW>
+__global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<PASSES>;
   constexpr int PLANES = C::PLANES, STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -186,7 +184,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], NUM_EPI_WARPS);
+      mbar_init(&cempty[s], EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapA)) : "memory");
@@ -320,9 +318,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 2..9)
+    // ---------------------------------------------------------------- epilogue (warps 2..)
+    // warp (quadrant q, sub s) owns TMEM lanes 32q..32q+31 and WC output columns
+    // WC*s .. WC*s+WC-1 of both Cr and Ci (WC = 64 with 8 warps, 32 with 16)
+    constexpr int WC = 512 / EW;
     const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) >> 2;           // output columns 64*half .. 64*half+63
+    const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const float scale = ldexpf(1.0f, -(*args.scaleA + *args.scaleB));
     float amax = 0.f;
@@ -331,15 +332,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
     for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
       int j, mt, nt;
       decode_tile(args, tile, j, mt, nt);
-      float sr[64], si[64];
+      float sr[WC], si[WC];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) { sr[i] = 0.f; si[i] = 0.f; }
+      for (int i = 0; i < WC; ++i) { sr[i] = 0.f; si[i] = 0.f; }
       for (int ch = 0; ch < nchunks; ++ch) {
         mbar_wait(&cfull[cb], cphase);
         fence_after();
-        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + cb * 256 + half * 64;
+        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + cb * 256 + half * WC;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < WC / 32; ++c) {
           uint32_t vr[32], vi[32];
           TN_LD32(vr, tb + c * 32);
           TN_LD32(vi, tb + 128 + c * 32);
@@ -359,12 +360,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
         }
       }
       const int m = mt * BM + row;
-      const int n0 = nt * BN + half * 64;
+      const int n0 = nt * BN + half * WC;
       if (m < args.M && n0 < args.N) {
         const int64_t base = ((int64_t)j * args.M + m) * (int64_t)args.N + n0;
         if (args.acc) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < WC; ++i) {
             if (n0 + i < args.N) {
               const float re = sr[i] * scale, im = si[i] * scale;
               double2 o = args.acc[base + i];
@@ -374,10 +375,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
               amax = fmaxf(amax, fmaxf(fabsf(re), fabsf(im)));
             }
           }
-        } else if ((args.N % 2) == 0 && n0 + 64 <= args.N) {
+        } else if ((args.N % 2) == 0 && n0 + WC <= args.N) {
           float4* dst = reinterpret_cast<float4*>(args.C + base);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < WC / 2; ++i) {
             const float r0 = sr[2 * i] * scale, i0 = si[2 * i] * scale;
             const float r1 = sr[2 * i + 1] * scale, i1 = si[2 * i + 1] * scale;
             dst[i] = make_float4(r0, i0, r1, i1);
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < WC; ++i) {
             if (n0 + i < args.N) {
               const float re = sr[i] * scale, im = si[i] * scale;
               args.C[base + i] = make_float2(re, im);
@@ -409,20 +410,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) cgemm_tcgen05_kernel(const __g
   }
 }
 
-template <int PASSES>
+template <int PASSES, int EW>
 cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
   static bool attr_set = false;
   const int smem = Cfg<PASSES>::SMEM_BYTES;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES>,
+    cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES, EW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
   if (grid < 1) grid = 1;
-  cgemm_tcgen05_kernel<PASSES><<<(unsigned)grid, NUM_THREADS, smem, s>>>(a);
+  cgemm_tcgen05_kernel<PASSES, EW><<<(unsigned)grid, 64 + 32 * EW, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+int epi_warps() {   // TN_GEMM_EPI = 8 | 16 epilogue warps
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TN_GEMM_EPI");
+    v = (e && atoi(e) == 16) ? 16 : 8;
+  }
+  return v;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -445,7 +455,9 @@ EncodeTiledFn get_encode() {
 }  // namespace
 
 cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s) {
-  return passes == 3 ? launch_impl<3>(a, num_sms, s) : launch_impl<1>(a, num_sms, s);
+  if (epi_warps() == 16)
+    return passes == 3 ? launch_impl<3, 16>(a, num_sms, s) : launch_impl<1, 16>(a, num_sms, s);
+  return passes == 3 ? launch_impl<3, 8>(a, num_sms, s) : launch_impl<1, 8>(a, num_sms, s);
 }
 
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,

@@ -311,15 +311,17 @@ __global__ void __launch_bounds__(256, 3) prep_gt_kernel(const PrepDesc* __restr
     spos[e] = gspos[e];
   }
   const int64_t plane = d.plane_elems;
-  __shared__ int64_t tile_off[2];
   for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
-    __syncthreads();   // tables ready / previous tile consumed
-    if (threadIdx.x == 0) {
-      tile_off[0] = decompose(c, d.nc, d.c_ext, d.c_src);
-      tile_off[1] = decompose(c, d.nc, d.c_ext, d.c_dst);
+    // outer tile offsets: shift decomposition, evaluated by every thread (no serial step)
+    int64_t sc = 0, dc = 0, t = c;
+    for (int i = d.nc - 1; i >= 0; --i) {
+      const int s = d.c_sh[i];
+      const int64_t digit = t & ((int64_t(1) << s) - 1);
+      t >>= s;
+      sc += digit * d.c_src[i];
+      dc += digit * d.c_dst[i];
     }
-    __syncthreads();
-    const int64_t sc = tile_off[0], dc = tile_off[1];
+    __syncthreads();   // tables ready / previous tile consumed
     for (int e = threadIdx.x; e < T; e += blockDim.x) tile[e] = src[sc + srcoff[e]];
     __syncthreads();
     for (int f = 2 * threadIdx.x; f < T; f += 2 * blockDim.x) {

@@ -319,13 +319,15 @@ int choose_prep_kind(tn::PrepDesc& p, int force) {
   }
   int64_t T = 1;
   for (auto& x : tl) T *= x.e;
-  while (T < 1024 && !pool.empty()) {             // amortise the per-tile overhead
+  while (T < 2048 && !pool.empty()) {             // amortise the per-tile overhead
     int q = 0;
     for (int i = 1; i < (int)pool.size(); ++i) if (pool[i].s < pool[q].s) q = i;
     const int64_t before = tl.size();
-    grab(q, (1024 + T - 1) / T);
+    grab(q, (2048 + T - 1) / T);
     T *= tl[before].e;
   }
+  for (auto& x : pool)
+    if (x.e & (x.e - 1)) return p.read_r_fast ? 0 : 1;   // outer dims use shift tables
   if (drun < 2 || drun % 2 != 0 || T > 4096 || T % 2 != 0 || (int)tl.size() > 12 ||
       (int)pool.size() > TN_MAXD)
     return p.read_r_fast ? 0 : 1;
@@ -349,6 +351,9 @@ int choose_prep_kind(tn::PrepDesc& p, int force) {
   p.nC = 1;
   for (int i = 0; i < p.nc; ++i) {
     p.c_ext[i] = pool[i].e; p.c_src[i] = pool[i].s; p.c_dst[i] = pool[i].t; p.nC *= pool[i].e;
+    int sh = 0;
+    while ((int64_t(1) << sh) < pool[i].e) ++sh;
+    p.c_sh[i] = (uint8_t)sh;
   }
   p.T = (int32_t)T;
   return 2;

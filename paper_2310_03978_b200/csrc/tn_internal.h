@@ -60,6 +60,7 @@ struct PrepDesc {
   int64_t td_ext[12];
   int32_t td_pos[12];                           // destination order, outer -> inner
   int64_t c_ext[TN_MAXD], c_src[TN_MAXD], c_dst[TN_MAXD];
+  uint8_t c_sh[TN_MAXD];          // log2 c_ext (general transposer requires power-of-two dims)
   const int64_t* gt_tab;          // plan-time tables: srcoff[T], dstoff[T], then int32 spos[T]
   __half* dst; int64_t plane_elems;
   const unsigned* absmax_in;      // absmax of the source tensor (float bits)
