@@ -322,10 +322,13 @@ __global__ void __launch_bounds__(256, 3) prep_gt_kernel(const PrepDesc* __restr
       dc += digit * d.c_dst[i];
     }
     __syncthreads();   // tables ready / previous tile consumed
-    for (int e = threadIdx.x; e < T; e += blockDim.x) tile[e] = src[sc + srcoff[e]];
+    // tile slot of source-order element e is swizzled (e ^ ((e >> 5) & 31)) so the
+    // strided destination-order reads spread over the banks
+    for (int e = threadIdx.x; e < T; e += blockDim.x) tile[e ^ ((e >> 5) & 31)] = src[sc + srcoff[e]];
     __syncthreads();
     for (int f = 2 * threadIdx.x; f < T; f += 2 * blockDim.x) {
-      const float2 v0 = tile[spos[f]], v1 = tile[spos[f + 1]];
+      const int p0 = spos[f], p1 = spos[f + 1];
+      const float2 v0 = tile[p0 ^ ((p0 >> 5) & 31)], v1 = tile[p1 ^ ((p1 >> 5) & 31)];
       const float xr0 = v0.x * scale, xi0 = v0.y * scale, xr1 = v1.x * scale, xi1 = v1.y * scale;
       const __half2 hr = __floats2half2_rn(xr0, xr1), hi = __floats2half2_rn(xi0, xi1);
       const int64_t idx = dc + dstoff[f];             // dstoff[f+1] = dstoff[f] + 1, idx even
