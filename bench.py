@@ -213,7 +213,16 @@ def run_ours(args):
         barrier()
         ms_local = e0.elapsed_time(e1)
         stats = ctx.kernel_stats()
+        step_ms = ctx.step_stats()
         ctx.set_profiling(False)
+    plan_steps = ctx.plan_json()["steps"]
+    top_steps = []
+    for s_ in np.argsort(-step_ms)[:8]:
+        p_ = plan_steps[int(s_)]
+        top_steps.append({"step": int(s_), "ms_per_slice": float(step_ms[s_]) / args.steps,
+                          "route": p_["route"] + ("/grouped" if p_.get("grouped") else ""),
+                          "J": p_["J"], "m": p_["m"], "n": p_["n"], "k": p_["k"],
+                          "tflops": p_["tcc"] * args.steps / max(step_ms[s_], 1e-9) / 1e9})
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
@@ -301,6 +310,7 @@ def run_ours(args):
                         "paper's 6.55e20 flop m=18 job / this run's aggregate TFLOPS"},
             "roofline": roofline,
             "kernel_stats": stats,
+            "top_steps": top_steps,
             "gpu_launches": launches,
             "clocks": clocks,
             "reduce_ms": reduce_ms,

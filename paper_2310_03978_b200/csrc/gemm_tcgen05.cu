@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
         int j, mt, nt;
         decode_tile(args, tile, j, mt, nt);
         const int sa = args.ia ? args.ia[j] : 0;
-        const int sb = args.ib ? args.ib[j] : 0;
+        const int sb = args.blk_slab_b ? args.blk_slab_b[mt] : (args.ib ? args.ib[j] : 0);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -359,10 +359,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
           cphase ^= 1;
         }
       }
-      const int m = mt * BM + row;
+      int m = mt * BM + row;
       const int n0 = nt * BN + half * WC;
-      if (m < args.M && n0 < args.N) {
-        const int64_t base = ((int64_t)j * args.M + m) * (int64_t)args.N + n0;
+      int64_t orow = (int64_t)j * args.M + m;
+      if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
+      if (m < args.M && n0 < args.N && orow >= 0) {
+        const int64_t base = orow * (int64_t)args.N + n0;
         if (args.acc) {
 #pragma unroll
           for (int i = 0; i < WC; ++i) {

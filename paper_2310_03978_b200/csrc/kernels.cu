@@ -259,8 +259,19 @@ __global__ void __launch_bounds__(256, 4) prep_direct_kernel(const PrepDesc* __r
     const int64_t kg = w % kgs, rg = w / kgs;
     const int64_t r = rg % d.R, g = rg / d.R;
     const int64_t k0 = kg * 8;
-    const int64_t base = g * d.g_stride + decompose(r, d.nr, d.r_ext, d.r_s);
     float2 v[8];
+    int64_t base;
+    if (d.rowoff) {                  // kind 3: gathered rows (slab-grouped merge)
+      base = d.rowoff[rg];
+      if (base < 0) {                // padding row
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = make_float2(0.f, 0.f);
+        split_store8<PLANES>(d, rg * d.Kpad + k0, v, scale);
+        continue;
+      }
+    } else {
+      base = g * d.g_stride + decompose(r, d.nr, d.r_ext, d.r_s);
+    }
     if (kvec && k0 + 8 <= d.K) {
       const float2* p = src + base + decompose(k0, d.nk, d.k_ext, d.k_s);
       if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
@@ -668,7 +679,7 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
       prep_gt_kernel<2><<<g, th, smem, s>>>(d_desc, leaf_off);
     return cudaGetLastError();
   }
-  if (kind == 1) {   // k-walking source: direct kernel, 8 elements per thread
+  if (kind == 1 || kind == 3) {   // k-walking source / gathered rows: 8 elements per thread
     const int g = grid_for(total / 8, th);
     if (planes == 4)
       prep_direct_kernel<4><<<g, th, 0, s>>>(d_desc, leaf_off);

@@ -82,6 +82,12 @@ struct StepPlan {
   // (tensor cores) / A side (SIMT general) / X outer dims (skinny); order2 = Q / B / Y
   std::vector<int64_t> order1, order2;
   tn::EinsumDesc hdesc;         // host copy of the SIMT descriptor (launch parameters)
+  // slab-grouped merge (tensor cores): the P side's rows are gathered (j, q) rows sorted
+  // by the Q side's slab, each slab group padded to 128 rows; see DESIGN.md "Sparse merges"
+  bool grouped = false;
+  int64_t g_rows = 0;           // gathered rows (multiple of 128)
+  std::vector<int32_t> g_rowmap, g_blk;   // output row of each gathered row; Q slab per block
+  int64_t g_rowmap_off = -1, g_blk_off = -1;
 };
 
 struct KStats {
@@ -93,6 +99,7 @@ struct Pending {
   cudaEvent_t a, b;
   int family;
   double flops, bytes;
+  int step;                     // path step the launch belongs to, -1 = none
 };
 
 }  // namespace
@@ -163,6 +170,7 @@ struct tn_ctx {
   bool profiling = false;
   std::vector<Pending> pending;
   KStats stats[4];
+  std::vector<double> step_ms;  // per path step (profiling)
 };
 
 namespace {
@@ -451,6 +459,9 @@ tn_status build_plan(tn_ctx* c) {
   const int tc_deep_k = env_int("TN_TC_DEEP_K", 1024);
   const int skinny_max_small = env_int("TN_SKINNY_MAX_SMALL", 64);
   const int prep_force = env_int("TN_PREP_FORCE", -1);   // tests: force a prep kernel kind
+  const int group_mode = env_int("TN_GROUP", 1);          // 0 off, 1 cost model, 2 always
+  const double group_max_bytes = 1e9 * env_int("TN_GROUP_MAX_GB", 32);
+  const int group_min_use = env_int("TN_GROUP_MIN_USE", 8);   // route when useful >= 1/this
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
 
@@ -594,6 +605,57 @@ tn_status build_plan(tn_ctx* c) {
             (small >= tc_small || sp.k >= tc_deep_k) && !sp.final_step &&
             sp.m < INT32_MAX && sp.n < INT32_MAX && sp.k < INT32_MAX && sp.J < INT32_MAX;
     sp.swap = sp.tc && sp.n > sp.m;   // tensor-core M side = larger free extent
+    if (sp.merge && sp.J > 1 && group_mode > 0 && !disable_tc && !sp.final_step &&
+        sp.k >= tc_k && sp.k < INT32_MAX) {
+      // Slab-grouped merge: with X the side whose slab is shared and Y the other, the
+      // batches j with slabX(j) = a form one GEMM  C[(j,y)][x] = Σ_k Y'[(j,y)][k] X[a][x][k]
+      // whose rows are Y's gathered rows.  Worth it when the per-batch tiles are mostly
+      // padding (a narrow free side) and the batches share few X slabs; it also moves
+      // merges too narrow per batch for the tensor cores onto them.
+      auto tiles_for = [&](const std::vector<int32_t>& sx, int64_t GX, int64_t P, int64_t Q,
+                           int64_t& rows) {
+        std::vector<int64_t> cnt((size_t)GX, 0);
+        for (int32_t a : sx) cnt[a]++;
+        rows = 0;
+        for (int64_t n_ : cnt) rows += (n_ * Q + 127) / 128 * 128;
+        return rows / 128 * ((P + 127) / 128);
+      };
+      int64_t rA = 0, rB = 0;
+      const int64_t tA = tiles_for(sp.ia, gA.ext, sp.m, sp.n, rA);   // X = A, Y = B
+      const int64_t tB = tiles_for(sp.ib, gB.ext, sp.n, sp.m, rB);   // X = B, Y = A
+      const int64_t cur = sp.J * ((sp.m + 127) / 128) * ((sp.n + 127) / 128);
+      const bool xa = tA <= tB;
+      const int64_t t = xa ? tA : tB, rows = xa ? rA : rB;
+      const int64_t kpad = (sp.k + 7) / 8 * 8;
+      // useful fraction of the grouped GEMM's MMA work
+      const double useful = (double)sp.J * sp.m * sp.n / ((double)t * 128.0 * 128.0);
+      const bool want = sp.tc ? (group_mode == 2 || 5 * t < 4 * cur)
+                              : (group_mode == 2 || useful * group_min_use >= 1.0);
+      if (want && rows < INT32_MAX &&
+          sp.J * (xa ? sp.n : sp.m) < INT32_MAX &&
+          (double)rows * kpad * 8.0 <= group_max_bytes) {
+        sp.grouped = true;
+        sp.tc = true;
+        sp.swap = xa;                 // tensor-core M side (prep side 0) = Y
+        sp.g_rows = rows;
+        const std::vector<int32_t>& sx = xa ? sp.ia : sp.ib;
+        const int64_t GX = xa ? gA.ext : gB.ext;
+        const int64_t Q = xa ? sp.n : sp.m;      // Y's free extent
+        std::vector<std::vector<int32_t>> members((size_t)GX);
+        for (int64_t j = 0; j < sp.J; ++j) members[sx[j]].push_back((int32_t)j);
+        sp.g_rowmap.assign((size_t)rows, -1);
+        sp.g_blk.assign((size_t)(rows / 128), 0);
+        int64_t r = 0;
+        for (int64_t a = 0; a < GX; ++a) {
+          if (members[a].empty()) continue;
+          const int64_t r0 = r;
+          for (int32_t j : members[a])
+            for (int64_t q = 0; q < Q; ++q) sp.g_rowmap[r++] = (int32_t)(j * Q + q);
+          r = r0 + ((r - r0) + 127) / 128 * 128;
+          for (int64_t b_ = r0 / 128; b_ < r / 128; ++b_) sp.g_blk[b_] = (int32_t)a;
+        }
+      }
+    }
 
     // output layout: [J][P dims][Q dims], P = A side unless swapped
     // SIMT mode (see kernels.cu): 2 = split-K dot, 1 = skinny (one small operand)
@@ -679,6 +741,12 @@ tn_status build_plan(tn_ctx* c) {
       sp.ib_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.ib.begin(), sp.ib.end());
     }
+    if (sp.grouped) {
+      sp.g_rowmap_off = (int64_t)tables.size();
+      tables.insert(tables.end(), sp.g_rowmap.begin(), sp.g_rowmap.end());
+      sp.g_blk_off = (int64_t)tables.size();
+      tables.insert(tables.end(), sp.g_blk.begin(), sp.g_blk.end());
+    }
     if (!sp.final_step) {
       sp.out_elems = out_elems;
       sp.out_off = arena.alloc(out_elems);
@@ -693,6 +761,10 @@ tn_status build_plan(tn_ctx* c) {
       sp.R[1] = sp.swap ? sp.m : sp.n;
       sp.G[0] = sp.merge ? (sp.swap ? gB.ext : gA.ext) : 1;
       sp.G[1] = sp.merge ? (sp.swap ? gA.ext : gB.ext) : 1;
+      if (sp.grouped) {   // side 0 = the gathered Y' rows, one slab
+        sp.R[0] = sp.g_rows;
+        sp.G[0] = 1;
+      }
       int64_t bytes0 = (4 * sp.G[0] * sp.R[0] * sp.Kpad * 2 + 1023) / 1024 * 1024;
       int64_t bytes1 = (4 * sp.G[1] * sp.R[1] * sp.Kpad * 2 + 1023) / 1024 * 1024;
       scratch = std::max(scratch, bytes0 + bytes1);
@@ -795,6 +867,7 @@ tn_status build_plan(tn_ctx* c) {
   std::vector<tn::PrepDesc> pds(std::max(n_prep, 1));
   std::vector<int64_t> gt_all;             // concatenated GT tables
   std::vector<std::pair<int, int64_t>> gt_ref;   // (prep index, offset in gt_all)
+  std::vector<std::pair<int, int64_t>> rw_ref;   // grouped-merge row tables, same pool
   auto base_of = [&](const View& v) -> const float2* { return v.buf == 0 ? c->d_leaf : c->d_arena; };
   // rebuild the live views to fill descriptors (same replay as above)
   live.clear();
@@ -953,7 +1026,26 @@ tn_status build_plan(tn_ctx* c) {
           const int64_t ks = p.nk ? p.k_s[p.nk - 1] : INT64_MAX;
           p.read_r_fast = rs < ks ? 1 : 0;
         }
-        {
+        if (sp.grouped && side == 0) {
+          // gathered rows: row r = (j, q) of the Y side -> slabY(j)·stride + offset of q
+          const std::vector<int32_t>& sy = fromA ? sp.ia : sp.ib;
+          const int64_t gys = fromA ? gA.stride : gB.stride;
+          const int64_t Q = fromA ? sp.m : sp.n;
+          std::vector<int64_t> rowoff((size_t)sp.g_rows, -1);
+          for (int64_t r = 0; r < sp.g_rows; ++r) {
+            const int32_t mrow = sp.g_rowmap[r];
+            if (mrow < 0) continue;
+            int64_t q = mrow % Q, off = (int64_t)sy[mrow / Q] * gys;
+            for (int d = p.nr - 1; d >= 0; --d) { off += (q % p.r_ext[d]) * p.r_s[d]; q /= p.r_ext[d]; }
+            rowoff[r] = off;
+          }
+          p.g_stride = 0;
+          p.kind = 3;
+          sp.r_fast[side] = 3;
+          sp.gtT[side] = 0;
+          rw_ref.push_back({sp.prep_idx + side, (int64_t)gt_all.size()});
+          gt_all.insert(gt_all.end(), rowoff.begin(), rowoff.end());
+        } else {
           const int64_t Kpad_ = sp.Kpad;
           p.Kpad = Kpad_;
           p.kind = choose_prep_kind(p, prep_force);
@@ -1004,6 +1096,16 @@ tn_status build_plan(tn_ctx* c) {
       g.tiles_m = (int32_t)((sp.R[0] + 127) / 128);
       g.tiles_n = (int32_t)((sp.R[1] + 127) / 128);
       g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * sp.J;
+      g.blk_slab_b = nullptr;
+      g.rowmap = nullptr;
+      if (sp.grouped) {   // one GEMM over the gathered rows; X slab per 128-row block
+        g.J = 1;
+        g.ia = nullptr;
+        g.ib = nullptr;
+        g.blk_slab_b = c->d_tables + sp.g_blk_off;
+        g.rowmap = c->d_tables + sp.g_rowmap_off;
+        g.n_tiles = (int64_t)g.tiles_m * g.tiles_n;
+      }
     }
     live.erase(sp.j);
     live[sp.i] = sp.out;
@@ -1019,6 +1121,7 @@ tn_status build_plan(tn_ctx* c) {
     if (st2) return st2;
     TN_CUDA(cudaMemcpyAsync(c->d_gt, gt_all.data(), gt_all.size() * 8, cudaMemcpyHostToDevice, sm));
     for (auto& r : gt_ref) pds[r.first].gt_tab = c->d_gt + r.second;
+    for (auto& r : rw_ref) pds[r.first].rowoff = c->d_gt + r.second;
   }
   if (n_prep) TN_CUDA(cudaMemcpyAsync(c->d_prep, pds.data(), n_prep * sizeof(tn::PrepDesc),
                                       cudaMemcpyHostToDevice, sm));
@@ -1033,8 +1136,10 @@ struct Timer {
   tn_ctx* c;
   int family;
   double flops, bytes;
+  int step;
   cudaEvent_t a{}, b{};
-  Timer(tn_ctx* c_, int f, double fl, double by) : c(c_), family(f), flops(fl), bytes(by) {
+  Timer(tn_ctx* c_, int f, double fl, double by, int st = -1)
+      : c(c_), family(f), flops(fl), bytes(by), step(st) {
     c->stats[f].launches++;
     if (c->profiling) {
       cudaEventCreate(&a);
@@ -1045,7 +1150,7 @@ struct Timer {
   ~Timer() {
     if (c->profiling) {
       cudaEventRecord(b, c->stream);
-      c->pending.push_back({a, b, family, flops, bytes});
+      c->pending.push_back({a, b, family, flops, bytes, step});
     }
   }
 };
@@ -1071,20 +1176,20 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
     for (size_t s = 0; s < c->steps.size(); ++s) {
       StepPlan& sp = c->steps[s];
       if (!sp.tc) {
-        Timer tm(c, 2, sp.tcc, sp.tmc);
+        Timer tm(c, 2, sp.tcc, sp.tmc, (int)s);
         TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm));
       } else {
         const int ps = passes[s];
         const int planes = ps == 3 ? 4 : 2;
         for (int side = 0; side < 2; ++side) {
-          Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes));
+          Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes), (int)s);
           TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
                                   sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm));
         }
         tn::GemmArgs ga = sp.gemm;
         ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
         ga.group_m = c->group_m;
-        Timer tm(c, 0, sp.tcc, sp.tmc);
+        Timer tm(c, 0, sp.tcc, sp.tmc, (int)s);
         TN_CUDA(tn::launch_gemm(ga, ps, c->num_sms, sm));
       }
     }
@@ -1455,13 +1560,21 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     char b[512];
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
-             "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"ia\":",
+             "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
+             "\"gathered_rows\":%lld,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
-             sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode);
+             sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
+             sp.grouped ? "true" : "false", (long long)sp.g_rows);
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";
     if (sp.merge) json_u64_list(o, sp.ib); else o += "null";
+    if (sp.grouped) {
+      o += ",\"g_rowmap\":";
+      json_u64_list(o, sp.g_rowmap);
+      o += ",\"g_blk\":";
+      json_u64_list(o, sp.g_blk);
+    }
     o += "}";
   }
   o += "],\"out_pos\":";
@@ -1485,21 +1598,36 @@ tn_status tn_set_profiling(tn_ctx* c, int enabled) {
   return TN_OK;
 }
 
+static tn_status drain_pending(tn_ctx* c) {
+  if (c->pending.empty()) return TN_OK;
+  TN_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->step_ms.size() < c->steps.size()) c->step_ms.resize(c->steps.size(), 0.0);
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    c->stats[p.family].ms += ms;
+    c->stats[p.family].flops += p.flops;
+    c->stats[p.family].bytes += p.bytes;
+    if (p.step >= 0 && p.step < (int)c->step_ms.size()) c->step_ms[p.step] += ms;
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  c->pending.clear();
+  return TN_OK;
+}
+
+tn_status tn_get_step_stats(tn_ctx* c, int64_t n, double* ms_out) {
+  if (!c || n < 0 || (n > 0 && !ms_out)) return fail(TN_ERR_USAGE, "bad arguments");
+  tn_status st = drain_pending(c);
+  if (st) return st;
+  for (int64_t s = 0; s < n; ++s) ms_out[s] = s < (int64_t)c->step_ms.size() ? c->step_ms[s] : 0.0;
+  return TN_OK;
+}
+
 tn_status tn_get_kernel_stats(tn_ctx* c, int family, tn_kernel_stats* out) {
   if (!c || family < 0 || family > 3 || !out) return fail(TN_ERR_USAGE, "bad arguments");
-  if (!c->pending.empty()) {
-    TN_CUDA(cudaStreamSynchronize(c->stream));
-    for (auto& p : c->pending) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, p.a, p.b);
-      c->stats[p.family].ms += ms;
-      c->stats[p.family].flops += p.flops;
-      c->stats[p.family].bytes += p.bytes;
-      cudaEventDestroy(p.a);
-      cudaEventDestroy(p.b);
-    }
-    c->pending.clear();
-  }
+  tn_status st = drain_pending(c);
+  if (st) return st;
   out->launches = c->stats[family].launches;
   out->ms = c->stats[family].ms;
   out->flops = c->stats[family].flops;
@@ -1512,6 +1640,7 @@ tn_status tn_reset_kernel_stats(tn_ctx* c) {
   tn_kernel_stats tmp;
   tn_get_kernel_stats(c, 0, &tmp);
   for (auto& s : c->stats) s = KStats();
+  c->step_ms.assign(c->steps.size(), 0.0);
   return TN_OK;
 }
 

@@ -62,6 +62,7 @@ struct PrepDesc {
   int64_t c_ext[TN_MAXD], c_src[TN_MAXD], c_dst[TN_MAXD];
   uint8_t c_sh[TN_MAXD];          // log2 c_ext (general transposer requires power-of-two dims)
   const int64_t* gt_tab;          // plan-time tables: srcoff[T], dstoff[T], then int32 spos[T]
+  const int64_t* rowoff;          // kind 3: source offset of each destination row (-1 = zeros)
   __half* dst; int64_t plane_elems;
   const unsigned* absmax_in;      // absmax of the source tensor (float bits)
   int* scale_out;                 // receives the exponent s (x * 2^s is split)
@@ -82,6 +83,11 @@ struct GemmArgs {
   int32_t kchunk;                 // k-blocks per TMEM chunk promoted to the fp32 RN
                                   // register sum (0 = whole K in TMEM); see DESIGN.md
   int32_t group_m;                // tile rasterization: tile rows per group (L2 reuse)
+  // grouped sparse merge (slab-regrouped Eq. 7): rows of A are gathered (j, q) rows
+  // sorted by B's slab; blk_slab_b[mt] = B slab of 128-row block mt; rowmap[r] = output
+  // row of gathered row r (-1 = padding); output C[rowmap[r]][n]
+  const int32_t* blk_slab_b;
+  const int32_t* rowmap;
 };
 
 // ---------------------------------------------------------------- slice select

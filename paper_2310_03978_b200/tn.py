@@ -24,7 +24,7 @@ _STATUS = {0: "TN_OK", 1: "TN_ERR_USAGE", 2: "TN_ERR_DATA", 3: "TN_ERR_RESOURCE"
 SYMBOLS = ["tn_create", "tn_load_network", "tn_upload_tensors", "tn_set_path", "tn_set_slices",
            "tn_contract", "tn_reset_accumulator", "tn_sum_slices", "tn_sum_slices_host",
            "tn_get_info", "tn_plan_json", "tn_set_profiling", "tn_get_kernel_stats",
-           "tn_reset_kernel_stats", "tn_cgemm", "tn_last_error", "tn_version", "tn_destroy"]
+           "tn_reset_kernel_stats", "tn_get_step_stats", "tn_cgemm", "tn_last_error", "tn_version", "tn_destroy"]
 
 
 class TNLibraryError(RuntimeError):
@@ -81,6 +81,7 @@ def lib():
         "tn_set_profiling": [VP, C.c_int],
         "tn_get_kernel_stats": [VP, C.c_int, P(KernelStats)],
         "tn_reset_kernel_stats": [VP],
+        "tn_get_step_stats": [VP, I64, VP],
         "tn_cgemm": [VP, VP, VP, VP, I64, I64, I64, I64, I64, I64, VP, VP, C.c_int, C.c_int],
     }
     for name, args in sig.items():
@@ -215,6 +216,13 @@ class Contraction:
             _check(lib().tn_get_kernel_stats(self._h, f, C.byref(k)))
             out[nm] = {"launches": k.launches, "ms": k.ms, "flops": k.flops, "bytes": k.bytes}
         return out
+
+    def step_stats(self) -> np.ndarray:
+        """Device ms per path step accumulated while profiling (tn_get_step_stats)."""
+        n = self.info()["n_steps"]
+        ms = np.zeros(n, np.float64)
+        _check(lib().tn_get_step_stats(self._h, n, _ptr(ms)))
+        return ms
 
     def reset_kernel_stats(self):
         _check(lib().tn_reset_kernel_stats(self._h))

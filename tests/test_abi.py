@@ -66,6 +66,29 @@ def test_plan_bookkeeping_raw_network_and_output_positions():
     assert pj["out_pos"] == [int(np.searchsorted(uniq, v)) for v in packed]
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_grouped_merge_tables(seed, monkeypatch):
+    """Slab-grouped merges: the gathered rows of every
+    grouped step cover each output row (j, q) exactly once, padding rows are -1, and
+    every 128-row block reads a single X slab, the one Eq. 7's table gives its j."""
+    for k, v in {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
+                 "TN_GROUP": "2"}.items():
+        monkeypatch.setenv(k, v)
+    w = configs.small(grid=(3, 4), cycles=8, mode="sparse", n_samples=64, n_slices=8, seed=seed)
+    c, pj = _check_plan(w)
+    grouped = [s for s in pj["steps"] if s["grouped"]]
+    assert grouped
+    for s in grouped:
+        Q = s["n"] if s["swap"] else s["m"]          # Y = tensor-core M side
+        sx = s["ia"] if s["swap"] else s["ib"]       # X slab of each merged config j
+        rm, blk = np.array(s["g_rowmap"]), np.array(s["g_blk"])
+        assert len(rm) == s["gathered_rows"] and len(rm) % 128 == 0 and len(blk) == len(rm) // 128
+        real = rm[rm >= 0]
+        assert np.array_equal(np.sort(real), np.arange(s["J"] * Q))
+        r = np.nonzero(rm >= 0)[0]
+        assert np.array_equal(np.array(sx)[rm[r] // Q], blk[r // 128])
+
+
 def test_c2_plan_matches_oracle_bookkeeping():
     w = configs.c2()
     c, pj = _check_plan(w)

@@ -132,6 +132,10 @@ ROUTES = {
                        "TN_PREP_FORCE": "1"},
     "tc_prep_general": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8",
                         "TN_PREP_FORCE": "2"},
+    "tc_grouped": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
+                   "TN_GROUP": "2"},
+    "tc_ungrouped": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                     "TN_GROUP": "0"},
     "default": {},
 }
 
@@ -151,6 +155,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
         c.setup(w.net, w.samples, w.path, w.sliced)
         modes = {s["mode"] for s in c.plan_json()["steps"]}
         assert ({1, 2} if route == "simt_modes" else {3}) <= modes, modes
+    if route == "tc_grouped" and mode == "sparse":
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        assert any(s["grouped"] for s in c.plan_json()["steps"])
     assert rel_l2(out, ref) <= EXT_TOL
     out_m, _ = run_gpu(ctx, w, precision="mixed", topk=10)
     assert rel_l2(out_m, ref) <= MIX_TOL
@@ -252,6 +260,7 @@ def test_c3_sparse_state_sampled_subnetwork(ctx):
     print(f"C3 sub-network: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
           f"max J {maxJ}, rel_l2 {err:.3e}")
     assert maxJ > 1000
+    assert any(s["grouped"] for s in pj["steps"])
     assert err <= EXT_TOL
 
 
