@@ -213,11 +213,11 @@ def run_ours(args):
         barrier()
         ms_local = e0.elapsed_time(e1)
         stats = ctx.kernel_stats()
-        step_ms = ctx.step_stats()
+        step_ms = ctx.step_stats(-1)
         ctx.set_profiling(False)
     plan_steps = ctx.plan_json()["steps"]
     top_steps = []
-    for s_ in np.argsort(-step_ms)[:8]:
+    for s_ in np.argsort(-step_ms)[:16]:
         p_ = plan_steps[int(s_)]
         top_steps.append({"step": int(s_), "ms_per_slice": float(step_ms[s_]) / args.steps,
                           "route": p_["route"] + ("/grouped" if p_.get("grouped") else ""),

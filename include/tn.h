@@ -162,11 +162,12 @@ typedef struct { int64_t launches; double ms; double flops; double bytes; } tn_k
 TN_API tn_status tn_get_kernel_stats(tn_ctx* ctx, int family, tn_kernel_stats* out);
 /* Zero all kernel-family statistics (synchronises pending profiling events). */
 TN_API tn_status tn_reset_kernel_stats(tn_ctx* ctx);
-/* Per path step: device milliseconds accumulated while profiling is enabled (prep +
- * GEMM, or the SIMT kernel, of step s), summed over the slices contracted since the
- * last reset.  ms_out: host array of n doubles (entries past the step count are 0).
- * Synchronises the context stream.  TN_ERR_USAGE on a null ctx or n < 0. */
-TN_API tn_status tn_get_step_stats(tn_ctx* ctx, int64_t n, double* ms_out);
+/* Per path step: device milliseconds accumulated while profiling is enabled, summed
+ * over the slices contracted since the last reset, for kernel family `family` (0 GEMM,
+ * 1 prep, 2 SIMT einsum, 3 misc) or all families (-1).  ms_out: host array of n
+ * doubles (entries past the step count are 0).  Synchronises the context stream.
+ * TN_ERR_USAGE on a null ctx, n < 0 or a bad family. */
+TN_API tn_status tn_get_step_stats(tn_ctx* ctx, int family, int64_t n, double* ms_out);
 
 /* Stand-alone complex GEMM through the same kernels (unit tests, accumulator
  * probes).  Device pointers, complex64 interleaved:

@@ -49,18 +49,29 @@ constexpr int BM = 128, BN = 128, BK = 32;          // BK in complex k (64 B fp1
 constexpr int PLANE_TILE = 128 * BK * 2;            // 8 KiB per plane tile
 constexpr uint32_t TMEM_COLS = 512;
 
-template <int PASSES>
+// PAIR = CTA pair (cta_group::2, cluster of 2): the MMA tile is 256 x 128; each CTA
+// stages its own 128 rows of A and half (64 rows) of B, so a CTA's smem supplies
+// 6 KiB per M=256 MMA instead of 8 KiB per M=128 MMA (smem bandwidth, not the
+// tensor pipe, bounds the single-CTA kernel: DESIGN.md "GEMM structure").
+template <int PASSES, bool PAIR = false>
 struct Cfg {
   static constexpr int PLANES = PASSES == 3 ? 4 : 2;
-  static constexpr int STAGE_BYTES = 2 * PLANES * PLANE_TILE;
-  static constexpr int STAGES = PASSES == 3 ? 3 : 6;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int B_TILE = PAIR ? PLANE_TILE / 2 : PLANE_TILE;   // per-plane B tile
+  static constexpr int STAGE_BYTES = PLANES * (PLANE_TILE + B_TILE);
+  static constexpr int STAGES = PAIR ? (PASSES == 3 ? 4 : 8) : (PASSES == 3 ? 3 : 6);
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BN * 8 /*column offsets*/;
+  static constexpr int TILE_M = PAIR ? 2 * BM : BM;
 };
 
 // instruction descriptor, kind::f16: D=f32 (bits 4-5 = 1), A=B=f16, K-major,
 // N>>3 at bits 17-22, M>>4 at bits 24-28; bit 13 = negate A.
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-constexpr uint32_t IDESC_NEG = IDESC | (1u << 13);
+template <bool PAIR>
+struct Idesc {
+  static constexpr uint32_t POS = (1u << 4) | ((uint32_t)(BN >> 3) << 17) |
+                                  ((uint32_t)((PAIR ? 2 * BM : BM) >> 4) << 24);
+  static constexpr uint32_t NEG = POS | (1u << 13);
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -85,6 +96,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// wait on a barrier that receives arrivals from the peer CTA (cluster-scope acquire)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nTN_WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra TN_WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// shared::cluster address of the same smem variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
@@ -95,6 +134,17 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* dst, u
       : "memory");
 }
 
+// CTA-pair TMA: the destination is this CTA's smem, the completion goes to the
+// leader CTA's barrier (bar_cluster = its shared::cluster address)
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, void* dst, uint32_t bar_cluster,
+                                                 int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // UMMA shared-memory descriptor, K-major, SWIZZLE_64B: 8-row atoms of 64 B rows,
 // SBO = 512 B between atoms, LBO unused (1), version 1 (sm_100), layout 4.
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
@@ -102,18 +152,35 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
-__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                    uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+template <bool PAIR>
+__device__ __forceinline__ void mma_t(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                      uint32_t accumulate) {
+  if constexpr (PAIR)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+// commit: arrive on `bar` when the issued MMAs retire (pair: on the barrier at the
+// same offset in both CTAs)
+template <bool PAIR>
+__device__ __forceinline__ void mma_commit_t(uint64_t* bar) {
+  if constexpr (PAIR)
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ void fence_before() {
@@ -159,10 +226,11 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int64_t tile, int
   }
 }
 
-template <int PASSES, int EW>
+template <int PASSES, int EW, bool PAIR>
 __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
-  using C = Cfg<PASSES>;
+  using C = Cfg<PASSES, PAIR>;
   constexpr int PLANES = C::PLANES, STAGES = C::STAGES;
+  constexpr uint32_t IDESC = Idesc<PAIR>::POS, IDESC_NEG = Idesc<PAIR>::NEG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
@@ -170,12 +238,18 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
   uint64_t* cfull = empty + STAGES;     // chunk accumulator ready (MMA -> epilogue)
   uint64_t* cempty = cfull + 2;         // chunk accumulator drained (epilogue -> MMA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+  // general output map: per-tile column offsets, double-buffered by tile parity
+  int64_t* noff_tab = reinterpret_cast<int64_t*>(smem + STAGES * C::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int kblocks = (args.K + BK - 1) / BK;
   const int kchunk = (args.kchunk > 0 && args.kchunk < kblocks) ? args.kchunk : kblocks;
   const int nchunks = (kblocks + kchunk - 1) / kchunk;
+  // pair: CTA rank in the cluster; tiles are scheduled per pair
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const int64_t unit = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
+  const int64_t units = PAIR ? (gridDim.x >> 1) : gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -184,44 +258,68 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], EW);
+      mbar_init(&cempty[s], PAIR ? 2 * EW : EW);   // pair: both CTAs' epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(PAIR ? &args.mapB2 : &args.mapB))
+                 : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------------- TMA producer
+      // pair: each CTA loads its own A rows and its half of B into its own smem;
+      // completion bytes of both CTAs go to the leader's full barrier
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
+      for (int64_t tile = unit; tile < args.n_tiles; tile += units) {
         int j, mt, nt;
         decode_tile(args, tile, j, mt, nt);
         const int sa = args.ia ? args.ia[j] : 0;
         const int sb = args.blk_slab_b ? args.blk_slab_b[mt] : (args.ib ? args.ib[j] : 0);
+        const int arow = mt * C::TILE_M + (int)rank * BM;
+        const int brow = nt * BN + (int)rank * (BN / 2);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* st = smem + stage * C::STAGE_BYTES;
+          if constexpr (PAIR) {
+            const uint32_t fb = map_rank(&full[stage], 0);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
 #pragma unroll
-          for (int p = 0; p < PLANES; ++p)
-            tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BK, mt * BM, sa, p);
+            for (int p = 0; p < PLANES; ++p)
+              tma_load_4d_pair(&args.mapA, st + p * PLANE_TILE, fb, kb * BK, arow, sa, p);
 #pragma unroll
-          for (int p = 0; p < PLANES; ++p)
-            tma_load_4d(&args.mapB, st + (PLANES + p) * PLANE_TILE, &full[stage], kb * BK, nt * BN,
-                        sb, p);
+            for (int p = 0; p < PLANES; ++p)
+              tma_load_4d_pair(&args.mapB2, st + PLANES * PLANE_TILE + p * C::B_TILE, fb, kb * BK,
+                               brow, sb, p);
+          } else {
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+#pragma unroll
+            for (int p = 0; p < PLANES; ++p)
+              tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BK, arow, sa, p);
+#pragma unroll
+            for (int p = 0; p < PLANES; ++p)
+              tma_load_4d(&args.mapB, st + PLANES * PLANE_TILE + p * C::B_TILE, &full[stage],
+                          kb * BK, brow, sb, p);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -230,17 +328,19 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       // ---------------------------------------------------------------- MMA issuer
       int stage = 0;
       uint32_t phase = 0;
       int cb = 0;
       uint32_t cphase = 0;
-      for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
+      for (int64_t tile = unit; tile < args.n_tiles; tile += units) {
         for (int kb = 0; kb < kblocks; ++kb) {
           const int kin = kb % kchunk;
           if (kin == 0) {
-            mbar_wait(&cempty[cb], cphase ^ 1);     // chunk buffer drained by the epilogue
+            // chunk buffer drained by the epilogue (pair: by both CTAs')
+            if constexpr (PAIR) mbar_wait_cluster(&cempty[cb], cphase ^ 1);
+            else mbar_wait(&cempty[cb], cphase ^ 1);
             fence_after();
           }
           const uint32_t d_re = tmem_base + cb * 256;
@@ -248,6 +348,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint32_t st = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb0 = st + PLANES * PLANE_TILE;
           if (PASSES == 3) {
             // Eq. 8, small terms first: every hi·lo / lo·hi MMA of the stage is
             // issued while the chunk accumulator is still ~2^-11 of its final size,
@@ -257,35 +358,35 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
               const uint32_t koff = kk * 32;   // 16 fp16 = 32 B along K inside the swizzle row
               const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
               const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
-              const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
-              const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
+              const uint64_t br = sdesc(sb0 + 0 * C::B_TILE + koff);
+              const uint64_t bi = sdesc(sb0 + 1 * C::B_TILE + koff);
               const uint64_t arl = sdesc(st + 2 * PLANE_TILE + koff);
               const uint64_t ail = sdesc(st + 3 * PLANE_TILE + koff);
-              const uint64_t brl = sdesc(st + (PLANES + 2) * PLANE_TILE + koff);
-              const uint64_t bil = sdesc(st + (PLANES + 3) * PLANE_TILE + koff);
+              const uint64_t brl = sdesc(sb0 + 2 * C::B_TILE + koff);
+              const uint64_t bil = sdesc(sb0 + 3 * C::B_TILE + koff);
               const uint32_t acc0 = (kin | kk) != 0;
               // real part: Ar·Br - Ai·Bi (cross terms)
-              mma(d_re, ar, brl, IDESC, acc0);
-              mma(d_re, arl, br, IDESC, 1);
-              mma(d_re, ail, bi, IDESC_NEG, 1);
-              mma(d_re, ai, bil, IDESC_NEG, 1);
+              mma_t<PAIR>(d_re, ar, brl, IDESC, acc0);
+              mma_t<PAIR>(d_re, arl, br, IDESC, 1);
+              mma_t<PAIR>(d_re, ail, bi, IDESC_NEG, 1);
+              mma_t<PAIR>(d_re, ai, bil, IDESC_NEG, 1);
               // imaginary part: Ar·Bi + Ai·Br (cross terms)
-              mma(d_im, ar, bil, IDESC, acc0);
-              mma(d_im, arl, bi, IDESC, 1);
-              mma(d_im, ai, brl, IDESC, 1);
-              mma(d_im, ail, br, IDESC, 1);
+              mma_t<PAIR>(d_im, ar, bil, IDESC, acc0);
+              mma_t<PAIR>(d_im, arl, bi, IDESC, 1);
+              mma_t<PAIR>(d_im, ai, brl, IDESC, 1);
+              mma_t<PAIR>(d_im, ail, br, IDESC, 1);
             }
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint32_t koff = kk * 32;
               const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
               const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
-              const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
-              const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
-              mma(d_re, ar, br, IDESC, 1);        // big·big last
-              mma(d_re, ai, bi, IDESC_NEG, 1);
-              mma(d_im, ar, bi, IDESC, 1);
-              mma(d_im, ai, br, IDESC, 1);
+              const uint64_t br = sdesc(sb0 + 0 * C::B_TILE + koff);
+              const uint64_t bi = sdesc(sb0 + 1 * C::B_TILE + koff);
+              mma_t<PAIR>(d_re, ar, br, IDESC, 1);        // big·big last
+              mma_t<PAIR>(d_re, ai, bi, IDESC_NEG, 1);
+              mma_t<PAIR>(d_im, ar, bi, IDESC, 1);
+              mma_t<PAIR>(d_im, ai, br, IDESC, 1);
             }
           } else {
 #pragma unroll
@@ -293,22 +394,22 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
               const uint32_t koff = kk * 32;
               const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
               const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
-              const uint64_t br = sdesc(st + (PLANES + 0) * PLANE_TILE + koff);
-              const uint64_t bi = sdesc(st + (PLANES + 1) * PLANE_TILE + koff);
+              const uint64_t br = sdesc(sb0 + 0 * C::B_TILE + koff);
+              const uint64_t bi = sdesc(sb0 + 1 * C::B_TILE + koff);
               const uint32_t acc0 = (kin | kk) != 0;
-              mma(d_re, ar, br, IDESC, acc0);
-              mma(d_re, ai, bi, IDESC_NEG, 1);
-              mma(d_im, ar, bi, IDESC, acc0);
-              mma(d_im, ai, br, IDESC, 1);
+              mma_t<PAIR>(d_re, ar, br, IDESC, acc0);
+              mma_t<PAIR>(d_re, ai, bi, IDESC_NEG, 1);
+              mma_t<PAIR>(d_im, ar, bi, IDESC, acc0);
+              mma_t<PAIR>(d_im, ai, br, IDESC, 1);
             }
           }
-          mma_commit(&empty[stage]);   // frees the smem stage when these MMAs retire
+          mma_commit_t<PAIR>(&empty[stage]);   // frees the smem stage(s) when these MMAs retire
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
           if (kin == kchunk - 1 || kb == kblocks - 1) {
-            mma_commit(&cfull[cb]);    // chunk accumulator ready for the epilogue
+            mma_commit_t<PAIR>(&cfull[cb]);    // chunk accumulator ready for the epilogue(s)
             if (++cb == 2) {
               cb = 0;
               cphase ^= 1;
@@ -329,7 +430,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
     float amax = 0.f;
     int cb = 0;
     uint32_t cphase = 0;
-    for (int64_t tile = blockIdx.x; tile < args.n_tiles; tile += gridDim.x) {
+    const uint32_t ce0 = PAIR ? map_rank(&cempty[0], 0) : 0;   // leader's drain barriers
+    const uint32_t ce1 = PAIR ? map_rank(&cempty[1], 0) : 0;
+    int titer = 0;
+    for (int64_t tile = unit; tile < args.n_tiles; tile += units, ++titer) {
       int j, mt, nt;
       decode_tile(args, tile, j, mt, nt);
       float sr[WC], si[WC];
@@ -353,14 +457,63 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
         }
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&cempty[cb]);
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_remote(cb ? ce1 : ce0);
+          else mbar_arrive(&cempty[cb]);
+        }
         if (++cb == 2) {
           cb = 0;
           cphase ^= 1;
         }
       }
-      int m = mt * BM + row;
+      int m = mt * C::TILE_M + (int)rank * BM + row;
       const int n0 = nt * BN + half * WC;
+      if (args.out_gen) {
+        // ---- general output map: column offsets of this tile into smem, then stores
+        int64_t* tab = noff_tab + (titer & 1) * BN;
+        const int et = threadIdx.x - 64;                 // epilogue thread 0 .. 32*EW-1
+        if (et < BN) {
+          int64_t t = (int64_t)nt * BN + et, off = 0;
+          for (int q = args.n_qo - 1; q >= 0; --q) {
+            const int sh = args.qo_sh[q];
+            off += (t & ((int64_t(1) << sh) - 1)) * args.qo_str[q];
+            t >>= sh;
+          }
+          tab[et] = off;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
+        if (m < args.M && n0 < args.N) {
+          int64_t t = m, moff = 0;
+          for (int q = args.n_po - 1; q >= 0; --q) {
+            const int sh = args.po_sh[q];
+            moff += (t & ((int64_t(1) << sh) - 1)) * args.po_str[q];
+            t >>= sh;
+          }
+          const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff;
+          const int64_t* tc = tab + half * WC;
+#pragma unroll
+          for (int i = 0; i < WC; i += 2) {      // full unroll: sr/si stay in registers
+            if (n0 + i >= args.N) continue;
+            const float r0 = sr[i] * scale, i0 = si[i] * scale;
+            const int64_t a0 = rb + tc[i];
+            amax = fmaxf(amax, fmaxf(fabsf(r0), fabsf(i0)));
+            if (n0 + i + 1 < args.N) {
+              const float r1 = sr[i + 1] * scale, i1 = si[i + 1] * scale;
+              const int64_t a1 = rb + tc[i + 1];
+              amax = fmaxf(amax, fmaxf(fabsf(r1), fabsf(i1)));
+              if (a1 == a0 + 1 && (a0 & 1) == 0) {
+                *reinterpret_cast<float4*>(args.C + a0) = make_float4(r0, i0, r1, i1);
+              } else {
+                args.C[a0] = make_float2(r0, i0);
+                args.C[a1] = make_float2(r1, i1);
+              }
+            } else {
+              args.C[a0] = make_float2(r0, i0);
+            }
+          }
+        }
+        continue;
+      }
       int64_t orow = (int64_t)j * args.M + m;
       if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
       if (m < args.M && n0 < args.N && orow >= 0) {
@@ -404,28 +557,54 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
     }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
   }
 }
 
-template <int PASSES, int EW>
+template <int PASSES, int EW, bool PAIR>
 cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
   static bool attr_set = false;
-  const int smem = Cfg<PASSES>::SMEM_BYTES;
+  const int smem = Cfg<PASSES, PAIR>::SMEM_BYTES;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES, EW>,
+    cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES, EW, PAIR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
-  if (grid < 1) grid = 1;
-  cgemm_tcgen05_kernel<PASSES, EW><<<(unsigned)grid, 64 + 32 * EW, smem, s>>>(a);
-  return cudaGetLastError();
+  if constexpr (PAIR) {
+    // tiles of 256 rows, one per CTA pair (cluster of 2); persistent over the SMs
+    GemmArgs p = a;
+    p.tiles_m = (a.M + 2 * BM - 1) / (2 * BM);
+    p.n_tiles = (int64_t)p.tiles_m * p.tiles_n * a.J;
+    int64_t pairs = p.n_tiles < num_sms / 2 ? p.n_tiles : num_sms / 2;
+    if (pairs < 1) pairs = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(64 + 32 * EW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, cgemm_tcgen05_kernel<PASSES, EW, PAIR>, p);
+  } else {
+    int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
+    if (grid < 1) grid = 1;
+    cgemm_tcgen05_kernel<PASSES, EW, PAIR><<<(unsigned)grid, 64 + 32 * EW, smem, s>>>(a);
+    return cudaGetLastError();
+  }
 }
 
 int epi_warps() {   // TN_GEMM_EPI = 8 | 16 epilogue warps
@@ -456,10 +635,23 @@ EncodeTiledFn get_encode() {
 
 }  // namespace
 
+int gemm_pair_min_m() {
+  const char* e = getenv("TN_GEMM_PAIR_MIN_M");
+  return e ? atoi(e) : 512;
+}
+
+bool gemm_pair_ok(const GemmArgs& a, int min_m) {
+  // the pair shares one B slab per 256-row tile: grouped merges (slab per 128-row
+  // block) stay on the single-CTA kernel
+  return min_m > 0 && a.M >= min_m && a.blk_slab_b == nullptr;
+}
+
 cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s) {
+  if (a.use_pair)
+    return passes == 3 ? launch_impl<3, 8, true>(a, num_sms, s) : launch_impl<1, 8, true>(a, num_sms, s);
   if (epi_warps() == 16)
-    return passes == 3 ? launch_impl<3, 16>(a, num_sms, s) : launch_impl<1, 16>(a, num_sms, s);
-  return passes == 3 ? launch_impl<3, 8>(a, num_sms, s) : launch_impl<1, 8>(a, num_sms, s);
+    return passes == 3 ? launch_impl<3, 16, false>(a, num_sms, s) : launch_impl<1, 16, false>(a, num_sms, s);
+  return passes == 3 ? launch_impl<3, 8, false>(a, num_sms, s) : launch_impl<1, 8, false>(a, num_sms, s);
 }
 
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,

@@ -88,6 +88,10 @@ struct StepPlan {
   int64_t g_rows = 0;           // gathered rows (multiple of 128)
   std::vector<int32_t> g_rowmap, g_blk;   // output row of each gathered row; Q slab per block
   int64_t g_rowmap_off = -1, g_blk_off = -1;
+  // tensor-core output map: the GEMM's row digits (P dims,
+  // order1) and column digits (Q dims, order2) with their strides in the output view
+  bool out_gen = false;
+  std::vector<VDim> po, qo;
 };
 
 struct KStats {
@@ -170,7 +174,7 @@ struct tn_ctx {
   bool profiling = false;
   std::vector<Pending> pending;
   KStats stats[4];
-  std::vector<double> step_ms;  // per path step (profiling)
+  std::vector<double> step_ms[4];  // per kernel family and path step (profiling)
 };
 
 namespace {
@@ -462,6 +466,8 @@ tn_status build_plan(tn_ctx* c) {
   const int group_mode = env_int("TN_GROUP", 1);          // 0 off, 1 cost model, 2 always
   const double group_max_bytes = 1e9 * env_int("TN_GROUP_MAX_GB", 32);
   const int group_min_use = env_int("TN_GROUP_MIN_USE", 8);   // route when useful >= 1/this
+  const int pair_min_m = tn::gemm_pair_min_m();            // CTA-pair GEMM for M >= this
+  const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
 
@@ -727,8 +733,45 @@ tn_status build_plan(tn_ctx* c) {
       std::vector<VDim> Q = sp.swap ? FA : FB;
       consumer_order(P, kc);
       consumer_order(Q, kc);
-      for (auto& d : P) { od.push_back({d.label, d.ext, 0}); sp.order1.push_back(d.label); }
-      for (auto& d : Q) { od.push_back({d.label, d.ext, 0}); sp.order2.push_back(d.label); }
+      for (auto& d : P) sp.order1.push_back(d.label);
+      for (auto& d : Q) sp.order2.push_back(d.label);
+      // tensor-core producers write [P keep][Q keep][contracted by the consumer, sorted
+      // by label]: the consumer's operand is then K-contiguous in the canonical (sorted)
+      // K order, so its prep is a streaming copy instead of a transpose
+      auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+      bool gen = sp.tc && !sp.grouped && out_layout && !kc.empty();
+      for (auto& d : P) gen = gen && p2(d.ext);
+      for (auto& d : Q) gen = gen && p2(d.ext);
+      if (gen) {
+        std::vector<VDim> con;
+        for (auto& d : P) (kc.count(d.label) ? con : od).push_back({d.label, d.ext, 0});
+        for (auto& d : Q) (kc.count(d.label) ? con : od).push_back({d.label, d.ext, 0});
+        std::sort(con.begin(), con.end(), [](const VDim& a, const VDim& b) { return a.label < b.label; });
+        od.insert(od.end(), con.begin(), con.end());
+        std::vector<VDim> tmp = od;
+        contiguous_strides(tmp);
+        auto ostride = [&](int64_t l) {
+          for (auto& d : tmp) if (d.label == l) return d.stride;
+          return (int64_t)0;
+        };
+        sp.po.clear();
+        sp.qo.clear();
+        for (auto& d : P) sp.po.push_back({d.label, d.ext, ostride(d.label)});
+        for (auto& d : Q) sp.qo.push_back({d.label, d.ext, ostride(d.label)});
+        coalesce1(sp.po);
+        coalesce1(sp.qo);
+        const bool plain = sp.po.size() <= 1 && sp.qo.size() == 1 && sp.qo[0].stride == 1 &&
+                           (sp.po.empty() || sp.po[0].stride == sp.qo[0].ext);
+        if (sp.po.size() > 16 || sp.qo.size() > 16 || plain) {
+          gen = false;     // plain [P][Q] layout (or too many dims): the fixed epilogue
+          od.resize(sp.merge ? 1 : 0);
+        }
+      }
+      sp.out_gen = gen;
+      if (!gen)
+        for (auto& d : P) od.push_back({d.label, d.ext, 0});
+      if (!gen)
+        for (auto& d : Q) od.push_back({d.label, d.ext, 0});
     }
     contiguous_strides(od);
     out.dims = od;
@@ -889,13 +932,23 @@ tn_status build_plan(tn_ctx* c) {
     std::vector<KDim> K;
     std::unordered_set<int64_t> kset;
     VDim gA{GROUP, 1, 0}, gB{GROUP, 1, 0};
-    for (auto& d : A.dims)
-      if (d.label != GROUP && lb.count(d.label)) {
-        kset.insert(d.label);
-        int64_t sb = 0;
-        for (auto& e : B.dims) if (e.label == d.label) sb = e.stride;
-        K.push_back({d.ext, d.stride, sb});
-      }
+    {
+      // canonical K order: sorted by label (tensor-core producers write their
+      // consumer's contracted bonds innermost in this order)
+      std::vector<std::pair<int64_t, KDim>> kl;
+      for (auto& d : A.dims)
+        if (d.label != GROUP && lb.count(d.label)) {
+          kset.insert(d.label);
+          int64_t sb = 0;
+          for (auto& e : B.dims) if (e.label == d.label) sb = e.stride;
+          kl.push_back({d.label, {d.ext, d.stride, sb}});
+        }
+      std::sort(kl.begin(), kl.end(),
+                [](const std::pair<int64_t, KDim>& a, const std::pair<int64_t, KDim>& b) {
+                  return a.first < b.first;
+                });
+      for (auto& x : kl) K.push_back(x.second);
+    }
     for (auto& d : A.dims) {
       if (d.label != GROUP && kset.count(d.label)) continue;
       if (sp.merge && d.label == GROUP) { gA = d; continue; }
@@ -1000,6 +1053,7 @@ tn_status build_plan(tn_ctx* c) {
       sp.hdesc = e;
     } else {
       // P operand = A side unless swapped; both share the canonical K order
+      memset(&sp.gemm, 0, sizeof(sp.gemm));
       for (int side = 0; side < 2; ++side) {
         const bool fromA = (side == 0) != sp.swap;
         const View& V = fromA ? A : B;
@@ -1067,8 +1121,10 @@ tn_status build_plan(tn_ctx* c) {
         sp.prep_total[side] = p.plane_elems;
         CUtensorMap* map = side == 0 ? &sp.gemm.mapA : &sp.gemm.mapB;
         if (!c->host_only &&
-            !tn::encode_plane_map(map, p.dst, sp.Kpad, sp.R[side], sp.G[side], 4, 128, errbuf,
-                                  sizeof(errbuf)))
+            (!tn::encode_plane_map(map, p.dst, sp.Kpad, sp.R[side], sp.G[side], 4, 128, errbuf,
+                                   sizeof(errbuf)) ||
+             (side == 1 && !tn::encode_plane_map(&sp.gemm.mapB2, p.dst, sp.Kpad, sp.R[side],
+                                                 sp.G[side], 4, 64, errbuf, sizeof(errbuf)))))
           return fail(TN_ERR_INTERNAL, errbuf);
         if (c->debug_plan) {
           fprintf(stderr, "[tn] step %d prep%c G=%lld R=%lld K=%lld kind=%d T=%d rows:", s,
@@ -1098,6 +1154,7 @@ tn_status build_plan(tn_ctx* c) {
       g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * sp.J;
       g.blk_slab_b = nullptr;
       g.rowmap = nullptr;
+      g.use_pair = 0;
       if (sp.grouped) {   // one GEMM over the gathered rows; X slab per 128-row block
         g.J = 1;
         g.ia = nullptr;
@@ -1105,6 +1162,15 @@ tn_status build_plan(tn_ctx* c) {
         g.blk_slab_b = c->d_tables + sp.g_blk_off;
         g.rowmap = c->d_tables + sp.g_rowmap_off;
         g.n_tiles = (int64_t)g.tiles_m * g.tiles_n;
+      }
+      g.use_pair = tn::gemm_pair_ok(g, pair_min_m) ? 1 : 0;
+      g.out_gen = sp.out_gen ? 1 : 0;
+      if (sp.out_gen) {
+        auto lg = [](int64_t x) { int q = 0; while ((int64_t(1) << q) < x) ++q; return q; };
+        g.n_po = (int32_t)sp.po.size();
+        g.n_qo = (int32_t)sp.qo.size();
+        for (int q = 0; q < g.n_po; ++q) { g.po_sh[q] = (uint8_t)lg(sp.po[q].ext); g.po_str[q] = sp.po[q].stride; }
+        for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)lg(sp.qo[q].ext); g.qo_str[q] = sp.qo[q].stride; }
       }
     }
     live.erase(sp.j);
@@ -1561,10 +1627,10 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
-             sp.grouped ? "true" : "false", (long long)sp.g_rows);
+             sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false");
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";
@@ -1601,14 +1667,15 @@ tn_status tn_set_profiling(tn_ctx* c, int enabled) {
 static tn_status drain_pending(tn_ctx* c) {
   if (c->pending.empty()) return TN_OK;
   TN_CUDA(cudaStreamSynchronize(c->stream));
-  if (c->step_ms.size() < c->steps.size()) c->step_ms.resize(c->steps.size(), 0.0);
+  for (auto& v : c->step_ms)
+    if (v.size() < c->steps.size()) v.resize(c->steps.size(), 0.0);
   for (auto& p : c->pending) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p.a, p.b);
     c->stats[p.family].ms += ms;
     c->stats[p.family].flops += p.flops;
     c->stats[p.family].bytes += p.bytes;
-    if (p.step >= 0 && p.step < (int)c->step_ms.size()) c->step_ms[p.step] += ms;
+    if (p.step >= 0 && p.step < (int)c->steps.size()) c->step_ms[p.family][p.step] += ms;
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
   }
@@ -1616,11 +1683,17 @@ static tn_status drain_pending(tn_ctx* c) {
   return TN_OK;
 }
 
-tn_status tn_get_step_stats(tn_ctx* c, int64_t n, double* ms_out) {
-  if (!c || n < 0 || (n > 0 && !ms_out)) return fail(TN_ERR_USAGE, "bad arguments");
+tn_status tn_get_step_stats(tn_ctx* c, int family, int64_t n, double* ms_out) {
+  if (!c || n < 0 || (n > 0 && !ms_out) || family < -1 || family > 3)
+    return fail(TN_ERR_USAGE, "bad arguments");
   tn_status st = drain_pending(c);
   if (st) return st;
-  for (int64_t s = 0; s < n; ++s) ms_out[s] = s < (int64_t)c->step_ms.size() ? c->step_ms[s] : 0.0;
+  for (int64_t s = 0; s < n; ++s) {
+    double v = 0.0;
+    for (int f = 0; f < 4; ++f)
+      if ((family < 0 || family == f) && s < (int64_t)c->step_ms[f].size()) v += c->step_ms[f][s];
+    ms_out[s] = v;
+  }
   return TN_OK;
 }
 
@@ -1640,7 +1713,7 @@ tn_status tn_reset_kernel_stats(tn_ctx* c) {
   tn_kernel_stats tmp;
   tn_get_kernel_stats(c, 0, &tmp);
   for (auto& s : c->stats) s = KStats();
-  c->step_ms.assign(c->steps.size(), 0.0);
+  for (auto& v : c->step_ms) v.assign(c->steps.size(), 0.0);
   return TN_OK;
 }
 
@@ -1704,7 +1777,8 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
       p[side].plane_elems = G * R * Kpad;
       p[side].absmax_in = am + side;
       p[side].scale_out = sc + side;
-      if (!tn::encode_plane_map(side ? &g.mapB : &g.mapA, p[side].dst, Kpad, R, G, 4, 128, err, sizeof(err))) {
+      if (!tn::encode_plane_map(side ? &g.mapB : &g.mapA, p[side].dst, Kpad, R, G, 4, 128, err, sizeof(err)) ||
+          (side == 1 && !tn::encode_plane_map(&g.mapB2, p[side].dst, Kpad, R, G, 4, 64, err, sizeof(err)))) {
         cudaFree(scr);
         return fail(TN_ERR_INTERNAL, err);
       }
@@ -1725,6 +1799,7 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * J;
     g.kchunk = passes == 3 ? c->kchunk3 : c->kchunk1;
     g.group_m = c->group_m;
+    g.use_pair = tn::gemm_pair_ok(g, tn::gemm_pair_min_m()) ? 1 : 0;
     {
       Timer tm(c, 0, 8.0 * (double)J * m * n * k, 8.0 * (double)(ga * m * k + gb * n * k + J * m * n));
       TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));

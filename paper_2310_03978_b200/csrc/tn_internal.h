@@ -72,6 +72,7 @@ struct PrepDesc {
 struct GemmArgs {
   CUtensorMap mapA;               // 4D fp16 (Kpad, R, G, planes), box (32, 128, 1, 1), SW64
   CUtensorMap mapB;
+  CUtensorMap mapB2;              // B with box (32, 64, 1, 1): per-CTA half of N for the CTA pair
   int32_t J, M, N, K;             // M = rows of A operand, N = rows of B operand (complex)
   const int32_t* ia; const int32_t* ib;
   float2* C;                      // [J][M][N] complex64
@@ -88,6 +89,14 @@ struct GemmArgs {
   // row of gathered row r (-1 = padding); output C[rowmap[r]][n]
   const int32_t* blk_slab_b;
   const int32_t* rowmap;
+  int32_t use_pair;               // 1: CTA-pair kernel (cta_group::2, 256-row tiles)
+  // general output map (out_gen = 1): C[j·M·N + Σ digit_p(m)·po_str[p] + Σ digit_q(n)·qo_str[q]]
+  // with row m / column n decomposed over power-of-two extents (log2 in po_sh / qo_sh,
+  // outer -> inner).  Lets the producer write the consumer's preferred layout
+  // ([P keep][Q keep][contracted, sorted]) so the consumer's operand is K-contiguous.
+  int32_t out_gen, n_po, n_qo, pad_o;
+  uint8_t po_sh[16], qo_sh[16];
+  int64_t po_str[16], qo_str[16];
 };
 
 // ---------------------------------------------------------------- slice select
@@ -112,6 +121,10 @@ cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* o
                               cudaStream_t s);
 cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s);
+// CTA-pair eligibility: M >= min_m (TN_GEMM_PAIR_MIN_M, default 512; 0 = never) and
+// one B slab per 256-row tile (not a grouped merge)
+bool gemm_pair_ok(const GemmArgs& a, int min_m);
+int gemm_pair_min_m();                   // reads TN_GEMM_PAIR_MIN_M
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
                       int planes, int box_rows, char* err, size_t errcap);
 

@@ -81,7 +81,7 @@ def lib():
         "tn_set_profiling": [VP, C.c_int],
         "tn_get_kernel_stats": [VP, C.c_int, P(KernelStats)],
         "tn_reset_kernel_stats": [VP],
-        "tn_get_step_stats": [VP, I64, VP],
+        "tn_get_step_stats": [VP, C.c_int, I64, VP],
         "tn_cgemm": [VP, VP, VP, VP, I64, I64, I64, I64, I64, I64, VP, VP, C.c_int, C.c_int],
     }
     for name, args in sig.items():
@@ -217,11 +217,12 @@ class Contraction:
             out[nm] = {"launches": k.launches, "ms": k.ms, "flops": k.flops, "bytes": k.bytes}
         return out
 
-    def step_stats(self) -> np.ndarray:
-        """Device ms per path step accumulated while profiling (tn_get_step_stats)."""
+    def step_stats(self, family: int = -1) -> np.ndarray:
+        """Device ms per path step accumulated while profiling (tn_get_step_stats);
+        family 0 GEMM, 1 prep, 2 SIMT, -1 all."""
         n = self.info()["n_steps"]
         ms = np.zeros(n, np.float64)
-        _check(lib().tn_get_step_stats(self._h, n, _ptr(ms)))
+        _check(lib().tn_get_step_stats(self._h, family, n, _ptr(ms)))
         return ms
 
     def reset_kernel_stats(self):

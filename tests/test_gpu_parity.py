@@ -56,10 +56,15 @@ def crandn(rng, *shape):
     (1, 300, 200, 100, 1, 1),     # ragged M, N, K tails, several tiles
     (1, 1024, 512, 2048, 1, 1),   # many tiles, deep K
     (5, 130, 70, 48, 3, 4),       # gather-batched (sparse einsum), tables
+    (3, 600, 200, 64, 2, 3),      # batched, M > 512 (pair kernel by default), ragged
     (1, 256, 16, 8, 1, 1),        # narrow N, K < BK
 ])
 @pytest.mark.parametrize("passes", [3, 1])
-def test_cgemm_tcgen05_vs_fp64(ctx, J, m, n, k, ga, gb, passes):
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_cgemm_tcgen05_vs_fp64(ctx, J, m, n, k, ga, gb, passes, pair, monkeypatch):
+    # pair "1": every GEMM on the CTA-pair kernel (cta_group::2, 256-row tiles, the
+    # second CTA's rows partly or wholly out of range for small m); "0": single CTA
+    monkeypatch.setenv("TN_GEMM_PAIR_MIN_M", pair)
     rng = np.random.default_rng(J * 1000 + m + n + k)
     A = crandn(rng, ga, m, k)
     B = crandn(rng, gb, n, k)
@@ -89,10 +94,12 @@ def test_cgemm_simt_vs_fp64(ctx):
     assert rel_l2(dC.cpu().numpy(), ref) < 1e-6
 
 
-def test_cgemm_exact_small_integers(ctx):
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_cgemm_exact_small_integers(ctx, pair, monkeypatch):
     """Integer-valued operands: every product and partial sum is exact in fp32,
     so the tensor-core result must be bit-exact (checks operand mapping, the
     negate bit and the re/im wiring independently of rounding)."""
+    monkeypatch.setenv("TN_GEMM_PAIR_MIN_M", pair)
     rng = np.random.default_rng(11)
     m, n, k = 192, 160, 96
     A = (rng.integers(-8, 9, (1, m, k)) + 1j * rng.integers(-8, 9, (1, m, k))).astype(np.complex64)
@@ -134,6 +141,12 @@ ROUTES = {
                         "TN_PREP_FORCE": "2"},
     "tc_grouped": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                    "TN_GROUP": "2"},
+    "tc_pair": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                "TN_GEMM_PAIR_MIN_M": "1"},
+    "tc_single_cta": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                      "TN_GEMM_PAIR_MIN_M": "0"},
+    "tc_old_layout": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                      "TN_OUT_LAYOUT": "0"},
     "tc_ungrouped": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
                      "TN_GROUP": "0"},
     "default": {},
@@ -155,6 +168,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
         c.setup(w.net, w.samples, w.path, w.sliced)
         modes = {s["mode"] for s in c.plan_json()["steps"]}
         assert ({1, 2} if route == "simt_modes" else {3}) <= modes, modes
+    if route == "tc":
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        assert any(s["out_gen"] for s in c.plan_json()["steps"])
     if route == "tc_grouped" and mode == "sparse":
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)

@@ -44,7 +44,7 @@ def main():
     err = float(np.linalg.norm(C[0, :64, :64].cpu().numpy() - ref) / np.linalg.norm(ref))
     res = {"m": m, "n": n, "k": k, "passes": a.passes, "ms_per_launch": st["ms"] / st["launches"],
            "tflops_useful": tflops, "tensor_tflops": tflops * a.passes, "rel_l2_block": err,
-           "env": {x: os.environ.get(x) for x in ("TN_KCHUNK3", "TN_GEMM_GROUP") if os.environ.get(x)}}
+           "env": {x: os.environ.get(x) for x in ("TN_KCHUNK3", "TN_GEMM_GROUP", "TN_GEMM_PAIR_MIN_M") if os.environ.get(x)}}
     print(json.dumps(res))
     if a.out:
         with open(a.out, "a") as f:
