@@ -354,6 +354,100 @@ __global__ void __launch_bounds__(256, 3) prep_gt_kernel(const PrepDesc* __restr
   }
 }
 
+// ---------------------------------------------------------------- operand prep, bit permutation
+// Every extent of a circuit network is a power of two, so an operand permutation
+// is a permutation of index bits: destination bit b carries source weight ws_b.
+// A tile is 2^t elements spanned by t bits holding the destination's innermost
+// bits (stored as 16-B plane vectors, walked in destination order) and the
+// source's smallest-weight bits (read as 16-B pairs, walked in source order);
+// the other bits enumerate tiles (outer weights in c_src / c_dst).  Tile offsets
+// come from plan-time tables that are separable in the index bits, and the smem
+// tile is XOR-swizzled per 16-slot row (mask chosen by the planner) so neither
+// phase has bank conflicts.  All loads of a tile are issued before any use:
+// 32 KB in flight per block, 4 blocks per SM.
+constexpr int BP_TMAX = 4096;
+constexpr size_t BP_SMEM = BP_TMAX * 8 + BP_TMAX / 8 * 8 + 128 * 8 + BP_TMAX * 2 + BP_TMAX / 16;
+
+template <int PLANES>
+__global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restrict__ gd,
+                                                         const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  float2* tile = reinterpret_cast<float2*>(dyn);                          // [TMAX] swizzled
+  int64_t* s_dst = reinterpret_cast<int64_t*>(tile + BP_TMAX);            // [TMAX/8]
+  int64_t* s_src = s_dst + BP_TMAX / 8;                                   // [128] lo | hi
+  uint16_t* s_slot = reinterpret_cast<uint16_t*>(s_src + 128);            // [TMAX]
+  uint8_t* s_m = reinterpret_cast<uint8_t*>(s_slot + BP_TMAX);            // [TMAX/16]
+  const int T = 1 << d.bp_t;
+  {
+    const int64_t* tab = d.bp_tab;
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) s_src[i] = tab[i];
+    for (int i = threadIdx.x; i < T / 8; i += blockDim.x) s_dst[i] = tab[128 + i];
+    const int64_t* ws = tab + 128 + T / 8;
+    for (int i = threadIdx.x; i < T / 4; i += blockDim.x)
+      reinterpret_cast<int64_t*>(s_slot)[i] = ws[i];
+    const int64_t* wm = ws + T / 4;
+    for (int i = threadIdx.x; i < (T / 16 + 7) / 8; i += blockDim.x)
+      reinterpret_cast<int64_t*>(s_m)[i] = wm[i];
+  }
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  const float scale = prep_scale(d);
+  const bool vec = d.bp_vec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  const int64_t tiles = d.G * d.nC;
+  const int64_t rk = d.R * d.Kpad;
+  for (int64_t c = blockIdx.x; c < tiles; c += gridDim.x) {
+    const int64_t g = c >> d.nc;                     // nC = 2^nc tiles per slab
+    const int64_t cc = c - (g << d.nc);
+    int64_t sc = g * d.g_stride, dc = g * rk;
+    for (int i = 0; i < d.nc; ++i)
+      if ((cc >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
+    __syncthreads();   // tables ready / previous tile consumed
+    const float2* sp = src + sc;
+    if (vec) {
+      float4 v[BP_TMAX / 512];
+#pragma unroll
+      for (int i = 0; i < BP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < T) v[i] = __ldg(reinterpret_cast<const float4*>(sp + s_src[e & 63] + s_src[64 + (e >> 6)]));
+      }
+#pragma unroll
+      for (int i = 0; i < BP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < T) *reinterpret_cast<float4*>(tile + (e ^ s_m[e >> 4])) = v[i];
+      }
+    } else {
+      float2 v[BP_TMAX / 256];
+#pragma unroll
+      for (int i = 0; i < BP_TMAX / 256; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < T) v[i] = __ldg(sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+      }
+#pragma unroll
+      for (int i = 0; i < BP_TMAX / 256; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < T) tile[e ^ s_m[e >> 4]] = v[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < BP_TMAX / 2048; ++i) {
+      const int q = threadIdx.x + i * 256;           // 8 destination-consecutive elements
+      if (q < T / 8) {
+        const uint4 sl = reinterpret_cast<const uint4*>(s_slot)[q];
+        const uint32_t w[4] = {sl.x, sl.y, sl.z, sl.w};
+        float2 v[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v[2 * j] = tile[w[j] & 0xFFFFu];
+          v[2 * j + 1] = tile[w[j] >> 16];
+        }
+        split_store8<PLANES>(d, dc + s_dst[q], v, scale);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- SIMT einsum, general
 // One thread per output C[j][m][n]; fp64 accumulation (a long fp32 RN chain would
 // cost ~2^-24·sqrt(K/2) relative).
@@ -663,6 +757,21 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
                         const int64_t* leaf_off, cudaStream_t s) {
   const int th = 256;
+  if (kind == 4) {   // bit-permutation transposer, tiles of tile_T <= 4096 elements
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(prep_bp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM);
+      cudaFuncSetAttribute(prep_bp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM);
+      attr = true;
+    }
+    const int64_t tiles = total / std::max(tile_T, 1);
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
+    if (planes == 4)
+      prep_bp_kernel<4><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off);
+    else
+      prep_bp_kernel<2><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off);
+    return cudaGetLastError();
+  }
   if (kind == 2) {   // general transposer, tiles of T <= 4096 elements
     static bool attr = false;
     if (!attr) {

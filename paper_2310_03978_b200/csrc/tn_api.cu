@@ -275,13 +275,132 @@ std::vector<VDim> arrange(const std::vector<VDim>& d, const std::vector<int64_t>
   return o;
 }
 
+// Bit-permutation transposer plan (prep kind 4, kernels.cu prep_bp_kernel).  With
+// every row / k extent a power of two and K = Kpad, destination element index bit
+// b (k bits innermost, then r bits) has a source weight ws_b.  The tile takes the
+// destination's innermost bits (>= 3: 8-element plane vectors) and the source's
+// smallest-weight bits; e (load order) sorts tile bits by source weight, f (store
+// order) by destination bit.  Fills the kind-4 fields and the tile tables.
+bool plan_bp(tn::PrepDesc& p, std::vector<int64_t>& tab) {
+  auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+  if (p.Kpad != p.K || p.K < 8 || !p2(p.K) || !p2(p.R) || p.rowoff) return false;
+  std::vector<int64_t> ws;
+  for (int d = p.nk - 1; d >= 0; --d) {
+    if (!p2(p.k_ext[d])) return false;
+    for (int64_t e = 1; e < p.k_ext[d]; e <<= 1) ws.push_back(e * p.k_s[d]);
+  }
+  for (int d = p.nr - 1; d >= 0; --d) {
+    if (!p2(p.r_ext[d])) return false;
+    for (int64_t e = 1; e < p.r_ext[d]; e <<= 1) ws.push_back(e * p.r_s[d]);
+  }
+  const int nb = (int)ws.size();
+  if (nb < 8 || nb - 8 > TN_MAXD) return false;
+  const int t = std::min(12, nb);
+  std::vector<int> bysrc(nb);
+  std::iota(bysrc.begin(), bysrc.end(), 0);
+  std::stable_sort(bysrc.begin(), bysrc.end(), [&](int a, int b) { return ws[a] < ws[b]; });
+  std::vector<char> in(nb, 0);
+  int cnt = 0;
+  auto add = [&](int b) { if (cnt < t && !in[b]) { in[b] = 1; ++cnt; } };
+  for (int b = 0; b < 3; ++b) add(b);                      // 8-element plane vectors
+  for (int i = 0; i < 6 && i < nb; ++i) add(bysrc[i]);     // source run (up to 512 B)
+  for (int b = 3; b < 6; ++b) add(b);                      // destination run (128 B / plane)
+  for (int i = 6; i < nb; ++i) add(bysrc[i]);              // more source locality
+  std::vector<int> ebit, fbit;                             // tile bits in e / f order
+  for (int i = 0; i < nb; ++i) if (in[bysrc[i]]) ebit.push_back(bysrc[i]);
+  for (int b = 0; b < nb; ++b) if (in[b]) fbit.push_back(b);
+  std::vector<int> epos(nb, -1);
+  for (int i = 0; i < t; ++i) epos[ebit[i]] = i;
+  const int T = 1 << t;
+  // swizzle: lanes of the store phase vary f bits 3..7; give each of their e
+  // positions >= 4 a distinct slot bit in {1,2,3} not already varied (bit 0 stays:
+  // pairs (e, e+1) are stored as one 16-B vector)
+  std::vector<int> mp(t, 0);
+  {
+    std::vector<char> used(4, 0);
+    for (int i = 3; i < 8 && i < t; ++i) if (epos[fbit[i]] < 4) used[epos[fbit[i]]] = 1;
+    for (int i = 3; i < 8 && i < t; ++i) {
+      const int pe = epos[fbit[i]];
+      if (pe < 4) continue;
+      for (int u = 1; u < 4; ++u)
+        if (!used[u]) { used[u] = 1; mp[pe] = 1 << u; break; }
+    }
+  }
+  std::vector<uint8_t> m(T / 16, 0);
+  for (int h = 0; h < T / 16; ++h)
+    for (int pe = 4; pe < t; ++pe) if ((h << 4) >> pe & 1) m[h] ^= (uint8_t)mp[pe];
+  tab.assign(128 + T / 8 + T / 4 + (T / 16 + 7) / 8, 0);
+  for (int x = 0; x < 64; ++x)
+    for (int i = 0; i < 6; ++i) {
+      if ((x >> i & 1) && i < t) tab[x] += ws[ebit[i]];
+      if ((x >> i & 1) && 6 + i < t) tab[64 + x] += ws[ebit[6 + i]];
+    }
+  for (int q = 0; q < T / 8; ++q)
+    for (int i = 3; i < t; ++i) if (q >> (i - 3) & 1) tab[128 + q] += int64_t(1) << fbit[i];
+  uint16_t* slot = reinterpret_cast<uint16_t*>(tab.data() + 128 + T / 8);
+  for (int f = 0; f < T; ++f) {
+    int e = 0;
+    for (int i = 0; i < t; ++i) if (f >> i & 1) e |= 1 << epos[fbit[i]];
+    slot[f] = (uint16_t)(e ^ m[e >> 4]);
+  }
+  memcpy(tab.data() + 128 + T / 8 + T / 4, m.data(), m.size());
+  p.nc = 0;
+  for (int b = 0; b < nb; ++b)
+    if (!in[b]) {
+      p.c_src[p.nc] = ws[b];
+      p.c_dst[p.nc] = int64_t(1) << b;
+      ++p.nc;
+    }
+  p.nC = int64_t(1) << p.nc;
+  bool vec = ws[ebit[0]] == 1 && (p.G == 1 || p.g_stride % 2 == 0);
+  for (int b = 0; b < nb; ++b) if (b != ebit[0] && ws[b] % 2 != 0) vec = false;
+  p.bp_vec = vec ? 1 : 0;
+  p.bp_t = t;
+  p.T = T;
+  // self-check (host, a few tiles): replay the kernel's load / store addressing and
+  // compare every element with the plain digit decomposition of its destination
+  {
+    std::vector<int> einv(T, -1);
+    for (int e = 0; e < T; ++e) {
+      const int sl = e ^ m[e >> 4];
+      if (sl < 0 || sl >= T || einv[sl] >= 0) return false;
+      einv[sl] = e;
+    }
+    auto ref_src = [&](int64_t di) {
+      const int64_t rk = p.R * p.K;
+      const int64_t g = di / rk;
+      int64_t r = (di % rk) / p.K, k = di % p.K, off = g * p.g_stride;
+      for (int d = p.nk - 1; d >= 0; --d) { off += (k % p.k_ext[d]) * p.k_s[d]; k /= p.k_ext[d]; }
+      for (int d = p.nr - 1; d >= 0; --d) { off += (r % p.r_ext[d]) * p.r_s[d]; r /= p.r_ext[d]; }
+      return off;
+    };
+    const int64_t tiles = p.G * p.nC;
+    for (int64_t c : {int64_t(0), int64_t(1), tiles / 3, tiles - 1}) {
+      if (c < 0 || c >= tiles) continue;
+      const int64_t g = c >> p.nc, cc = c - (g << p.nc);
+      int64_t sc = g * p.g_stride, dc = g * p.R * p.Kpad;
+      for (int i = 0; i < p.nc; ++i) if ((cc >> i) & 1) { sc += p.c_src[i]; dc += p.c_dst[i]; }
+      for (int f = 0; f < T; ++f) {
+        const int e = einv[slot[f]];
+        const int64_t so = sc + tab[e & 63] + tab[64 + (e >> 6)];
+        const int64_t di = dc + tab[128 + (f >> 3)] + (f & 7);
+        if (so != ref_src(di)) return false;
+      }
+    }
+  }
+  return true;
+}
+
 // Operand-prep kernel choice: 1 = direct (source walks k with a
-// contiguous innermost k run of >= 8), 2 = general transposer (blocks: the
-// destination's contiguous k-run x the source's innermost run), 0 = r/k tile
-// transposer (fallback).  Fills the general-transposer fields.
-int choose_prep_kind(tn::PrepDesc& p, int force) {
+// contiguous innermost k run of >= 8), 4 = bit-permutation transposer (power-of-
+// two extents), 2 = general transposer (blocks: the destination's contiguous
+// k-run x the source's innermost run), 0 = r/k tile transposer (fallback).
+// Fills the transposer fields; `tab` receives kind 2 / 4 tile tables.
+int choose_prep_kind(tn::PrepDesc& p, int force, std::vector<int64_t>& tab) {
   if (force == 0 || force == 1) return force;
-  if (force != 2 && p.nk > 0 && p.k_s[p.nk - 1] == 1 && p.k_ext[p.nk - 1] % 8 == 0) return 1;
+  if (force != 2 && force != 4 && p.nk > 0 && p.k_s[p.nk - 1] == 1 && p.k_ext[p.nk - 1] % 8 == 0) return 1;
+  static const int bp_on = getenv("TN_PREP_BP") ? atoi(getenv("TN_PREP_BP")) : 1;
+  if (force != 2 && (bp_on || force == 4) && plan_bp(p, tab)) return 4;
   if (p.K % 8 != 0 || p.Kpad != p.K || (force != 2 && p.G * p.R * p.K < 2048))
     return p.read_r_fast ? 0 : 1;
   struct D { int64_t e, s, t; };
@@ -911,6 +1030,7 @@ tn_status build_plan(tn_ctx* c) {
   std::vector<int64_t> gt_all;             // concatenated GT tables
   std::vector<std::pair<int, int64_t>> gt_ref;   // (prep index, offset in gt_all)
   std::vector<std::pair<int, int64_t>> rw_ref;   // grouped-merge row tables, same pool
+  std::vector<std::pair<int, int64_t>> bp_ref;   // bit-permutation tile tables, same pool
   auto base_of = [&](const View& v) -> const float2* { return v.buf == 0 ? c->d_leaf : c->d_arena; };
   // rebuild the live views to fill descriptors (same replay as above)
   live.clear();
@@ -1102,12 +1222,13 @@ tn_status build_plan(tn_ctx* c) {
         } else {
           const int64_t Kpad_ = sp.Kpad;
           p.Kpad = Kpad_;
-          p.kind = choose_prep_kind(p, prep_force);
+          std::vector<int64_t> tab;
+          p.kind = choose_prep_kind(p, prep_force, tab);
           sp.r_fast[side] = p.kind;
-          sp.gtT[side] = p.kind == 2 ? p.T : 0;
-          if (p.kind == 2) {
-            std::vector<int64_t> tab = gt_tables(p);
-            gt_ref.push_back({sp.prep_idx + side, (int64_t)gt_all.size()});
+          sp.gtT[side] = (p.kind == 2 || p.kind == 4) ? p.T : 0;
+          if (p.kind == 2) tab = gt_tables(p);
+          if (p.kind == 2 || p.kind == 4) {
+            (p.kind == 2 ? gt_ref : bp_ref).push_back({sp.prep_idx + side, (int64_t)gt_all.size()});
             gt_all.insert(gt_all.end(), tab.begin(), tab.end());
           }
         }
@@ -1188,6 +1309,7 @@ tn_status build_plan(tn_ctx* c) {
     TN_CUDA(cudaMemcpyAsync(c->d_gt, gt_all.data(), gt_all.size() * 8, cudaMemcpyHostToDevice, sm));
     for (auto& r : gt_ref) pds[r.first].gt_tab = c->d_gt + r.second;
     for (auto& r : rw_ref) pds[r.first].rowoff = c->d_gt + r.second;
+    for (auto& r : bp_ref) pds[r.first].bp_tab = c->d_gt + r.second;
   }
   if (n_prep) TN_CUDA(cudaMemcpyAsync(c->d_prep, pds.data(), n_prep * sizeof(tn::PrepDesc),
                                       cudaMemcpyHostToDevice, sm));
@@ -1627,10 +1749,11 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"out_gen\":%s,\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
-             sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false");
+             sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false",
+             sp.tc ? sp.r_fast[0] : -1, sp.tc ? sp.r_fast[1] : -1);
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";

@@ -63,6 +63,11 @@ struct PrepDesc {
   uint8_t c_sh[TN_MAXD];          // log2 c_ext (general transposer requires power-of-two dims)
   const int64_t* gt_tab;          // plan-time tables: srcoff[T], dstoff[T], then int32 spos[T]
   const int64_t* rowoff;          // kind 3: source offset of each destination row (-1 = zeros)
+  // bit-permutation transposer (kind 4): tile of 2^bp_t elements; outer bits in c_src /
+  // c_dst (nc of them, nC = 2^nc tiles per slab); bp_tab = plan-time tile tables
+  // [src lo/hi 128][dst T/8][slot T/4 words of u16][swizzle T/128 words of u8]
+  int32_t bp_t, bp_vec;           // bp_vec: source pairs (e, e+1) are adjacent (16-B loads)
+  const int64_t* bp_tab;
   __half* dst; int64_t plane_elems;
   const unsigned* absmax_in;      // absmax of the source tensor (float bits)
   int* scale_out;                 // receives the exponent s (x * 2^s is split)
