@@ -96,24 +96,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// wait on a barrier that receives arrivals from the peer CTA (cluster-scope acquire)
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred P1;\nTN_WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra TN_WAITC_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 // shared::cluster address of the same smem variable in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Arrive on a barrier of another CTA of the cluster.  Only TMEM reads are ordered
+// by this arrive (tcgen05.wait::ld + fence::before_thread_sync precede it), so the
+// default CTA-scope release suffices; a cluster-scope release compiles to a
+// MEMBAR.ALL.GPU + ERRBAR per drained chunk (43 % of the epilogue's stall samples).
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -152,35 +146,41 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
+// MMA issue: called by the whole (converged) MMA warp; one lane is elected inside
+// the asm, so every operand stays warp-uniform (uniform registers, no per-MMA
+// ELECT / R2UR.BROADCAST loop as when a single-lane branch issues it).
 template <bool PAIR>
 __device__ __forceinline__ void mma_t(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                       uint32_t accumulate) {
   if constexpr (PAIR)
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
   else
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-// commit: arrive on `bar` when the issued MMAs retire (pair: on the barrier at the
-// same offset in both CTAs)
+// commit (elected lane of the converged MMA warp): arrive on `bar` when the issued
+// MMAs retire (pair: on the barrier at the same offset in both CTAs)
 template <bool PAIR>
 __device__ __forceinline__ void mma_commit_t(uint64_t* bar) {
   if constexpr (PAIR)
     asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n}" ::"r"(smem_u32(bar)),
         "h"((uint16_t)3)
         : "memory");
   else
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+            smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void fence_before() {
@@ -328,8 +328,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
       // ---------------------------------------------------------------- MMA issuer
+      // (whole warp, converged; one elected lane issues each tcgen05 instruction)
       int stage = 0;
       uint32_t phase = 0;
       int cb = 0;
@@ -339,8 +340,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
           const int kin = kb % kchunk;
           if (kin == 0) {
             // chunk buffer drained by the epilogue (pair: by both CTAs')
-            if constexpr (PAIR) mbar_wait_cluster(&cempty[cb], cphase ^ 1);
-            else mbar_wait(&cempty[cb], cphase ^ 1);
+            mbar_wait(&cempty[cb], cphase ^ 1);   // pair: arrivals from both CTAs' epilogues
             fence_after();
           }
           const uint32_t d_re = tmem_base + cb * 256;

@@ -492,121 +492,81 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
 
 // ---------------------------------------------------------------- SIMT einsum, skinny
 // C[o][n][v] = Σ_k A[o, v, k] B[n, k] for a small B (N*K <= 8192 complex, staged
-// in smem once per block) and a big A streamed exactly once: lanes walk A's
-// smallest-stride free dim v (coalesced reads), the output keeps v innermost
-// (coalesced writes).  These are the HBM-bound "absorb a gate into the stem"
-// steps (stage 1 dominates).  fp32 accumulation (K <= 64 here).
-template <int NMAX, bool POW2>
+// in smem once per block, rows padded to an even N) and a big A streamed exactly
+// once: lanes walk A's smallest-stride free dim v (coalesced reads), the output
+// keeps v innermost (coalesced writes).  These are the HBM-bound "absorb a gate
+// into the stem" steps (stage 1 dominates).  VEC = 2: a thread
+// owns the pair (v, v+1) (unit-stride, even run): 16-B loads and stores.  The k
+// loop issues KU loads before any use (memory-level parallelism), and B is read
+// as 16-B pairs of n, so one shared-memory load feeds 8·VEC FMAs.  fp32
+// accumulation (K <= 256 here).
+template <int NMAX, int VEC, bool POW2>
 __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __restrict__ gd,
                                                             const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) EinsumDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
-  const int K = (int)d.K, N = (int)d.N;
-  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][N]
-  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * N);
+  const int K = (int)d.K, N = (int)d.N, Np = (N + 1) & ~1;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][Np]
+  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * Np);
   const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
   const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
-  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
-    const int k = e / N, n = e % N;
-    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  for (int e = threadIdx.x; e < K * Np; e += blockDim.x) {
+    const int k = e / Np, n = e % Np;
+    Bs[e] = n < N ? B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)]
+                  : make_float2(0.f, 0.f);
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
   __syncthreads();
-  const int64_t V = d.V;
+  constexpr int KU = NMAX <= 16 ? 8 : 4;
+  const int64_t V = d.V, Vv = V / VEC, Mv = d.M / VEC;
   const int64_t vstride = d.m_sa[d.nm - 1];
-  // U rows per thread per iteration (independent loads in flight); U = 2 while
-  // the accumulators fit comfortably in registers
-  constexpr int U = NMAX <= 16 ? 2 : 1;
-  const int64_t step = (int64_t)gridDim.x * blockDim.x;
   float amax = 0.f;
-  for (int64_t m0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m0 < d.M; m0 += U * step) {
-    const float2* a_row[U];
-    int64_t obase[U];
-    bool live[U];
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mv;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t vi = (m % Vv) * VEC, o = m / Vv;
+    const float2* a_row = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
+                                    : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
+    float cr[VEC][NMAX], ci[VEC][NMAX];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t m = m0 + u * step;
-      live[u] = m < d.M;
-      const int64_t mm = live[u] ? m : m0;
-      const int64_t vi = mm % V, o = mm / V;
-      a_row[u] = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
-                           : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
-      obase[u] = o * N * V + vi;
-    }
-    float accr[U][NMAX], acci[U][NMAX];
+    for (int u = 0; u < VEC; ++u)
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+      for (int n = 0; n < NMAX; ++n) { cr[u][n] = 0.f; ci[u][n] = 0.f; }
+    for (int k0 = 0; k0 < K; k0 += KU) {
+      float2 a[KU][VEC];
 #pragma unroll
-      for (int n = 0; n < NMAX; ++n) { accr[u][n] = 0.f; acci[u][n] = 0.f; }
-    for (int k = 0; k < K; ++k) {
-      float2 a[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) a[u] = a_row[u][koff[k]];
-#pragma unroll
-      for (int n = 0; n < NMAX; ++n) {
-        if (n < N) {
-          const float2 b = Bs[k * N + n];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            accr[u][n] = fmaf(a[u].x, b.x, accr[u][n]);
-            accr[u][n] = fmaf(-a[u].y, b.y, accr[u][n]);
-            acci[u][n] = fmaf(a[u].x, b.y, acci[u][n]);
-            acci[u][n] = fmaf(a[u].y, b.x, acci[u][n]);
+      for (int kk = 0; kk < KU; ++kk) {
+        if (k0 + kk < K) {
+          if (VEC == 2) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(a_row + koff[k0 + kk]));
+            a[kk][0] = make_float2(q.x, q.y);
+            a[kk][VEC - 1] = make_float2(q.z, q.w);
+          } else {
+            a[kk][0] = __ldg(a_row + koff[k0 + kk]);
           }
+        } else {
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) a[kk][u] = make_float2(0.f, 0.f);
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (live[u])
+      for (int kk = 0; kk < KU; ++kk) {
+        if (k0 + kk < K) {
+          const float4* brow = reinterpret_cast<const float4*>(Bs + (k0 + kk) * Np);
 #pragma unroll
-        for (int n = 0; n < NMAX; ++n)
-          if (n < N) store_out_f(d, obase[u] + (int64_t)n * V, accr[u][n], acci[u][n], amax);
-  }
-  if (d.absmax_out) block_absmax(amax, d.absmax_out);
-}
-
-// Vectorised variant: the lane run v is unit-stride and even, so a thread owns the
-// pair (v, v+1): one 16-byte load per k and one 16-byte store per n (pairs are
-// adjacent in A and in C), half the instructions per byte of the scalar kernel.
-template <int NMAX, bool POW2>
-__global__ void __launch_bounds__(256) einsum_skinny2_kernel(const EinsumDesc* __restrict__ gd,
-                                                             const int64_t* __restrict__ leaf_off) {
-  __shared__ __align__(16) EinsumDesc d;
-  copy_desc_to_smem(&d, gd);
-  extern __shared__ __align__(16) uint8_t dyn[];
-  const int K = (int)d.K, N = (int)d.N;
-  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][N]
-  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * N);
-  const float2* A = d.A + d.a_off;
-  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
-  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
-    const int k = e / N, n = e % N;
-    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
-  }
-  for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
-  __syncthreads();
-  const int64_t V = d.V, Vh = V / 2, Mh = d.M / 2;
-  float amax = 0.f;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mh;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = (m % Vh) * 2, o = m / Vh;
-    const float2* a_row = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
-                                    : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi;
-    float r0[NMAX], i0[NMAX], r1[NMAX], i1[NMAX];
+          for (int n2 = 0; n2 < NMAX / 2; ++n2) {
+            if (2 * n2 < N) {
+              const float4 b = brow[n2];     // B[2n2] = (x, y), B[2n2+1] = (z, w)
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) { r0[n] = 0.f; i0[n] = 0.f; r1[n] = 0.f; i1[n] = 0.f; }
-    for (int k = 0; k < K; ++k) {
-      const float4 q = *reinterpret_cast<const float4*>(a_row + koff[k]);
-#pragma unroll
-      for (int n = 0; n < NMAX; ++n) {
-        if (n < N) {
-          const float2 b = Bs[k * N + n];
-          r0[n] = fmaf(q.x, b.x, r0[n]); r0[n] = fmaf(-q.y, b.y, r0[n]);
-          i0[n] = fmaf(q.x, b.y, i0[n]); i0[n] = fmaf(q.y, b.x, i0[n]);
-          r1[n] = fmaf(q.z, b.x, r1[n]); r1[n] = fmaf(-q.w, b.y, r1[n]);
-          i1[n] = fmaf(q.z, b.y, i1[n]); i1[n] = fmaf(q.w, b.x, i1[n]);
+              for (int u = 0; u < VEC; ++u) {
+                const float2 x = a[kk][u];
+                cr[u][2 * n2] = fmaf(x.x, b.x, fmaf(-x.y, b.y, cr[u][2 * n2]));
+                ci[u][2 * n2] = fmaf(x.x, b.y, fmaf(x.y, b.x, ci[u][2 * n2]));
+                cr[u][2 * n2 + 1] = fmaf(x.x, b.z, fmaf(-x.y, b.w, cr[u][2 * n2 + 1]));
+                ci[u][2 * n2 + 1] = fmaf(x.x, b.w, fmaf(x.y, b.z, ci[u][2 * n2 + 1]));
+              }
+            }
+          }
         }
       }
     }
@@ -615,12 +575,13 @@ __global__ void __launch_bounds__(256) einsum_skinny2_kernel(const EinsumDesc* _
     for (int n = 0; n < NMAX; ++n) {
       if (n < N) {
         const int64_t idx = base + (int64_t)n * V;
-        if (d.acc) {
-          store_out_f(d, idx, r0[n], i0[n], amax);
-          store_out_f(d, idx + 1, r1[n], i1[n], amax);
+        if (VEC == 2 && !d.acc) {
+          *reinterpret_cast<float4*>(d.C + idx) = make_float4(cr[0][n], ci[0][n], cr[VEC - 1][n], ci[VEC - 1][n]);
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(cr[0][n]), fabsf(ci[0][n])),
+                                   fmaxf(fabsf(cr[VEC - 1][n]), fabsf(ci[VEC - 1][n]))));
         } else {
-          *reinterpret_cast<float4*>(d.C + idx) = make_float4(r0[n], i0[n], r1[n], i1[n]);
-          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0[n]), fabsf(i0[n])), fmaxf(fabsf(r1[n]), fabsf(i1[n]))));
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) store_out_f(d, idx + u, cr[u][n], ci[u][n], amax);
         }
       }
     }
@@ -631,46 +592,74 @@ __global__ void __launch_bounds__(256) einsum_skinny2_kernel(const EinsumDesc* _
 // ---------------------------------------------------------------- SIMT einsum, wide skinny
 // Same layout contract as einsum_skinny_kernel (out [Mo][N][V]) for outer-product-
 // like steps: K <= KMAX (the big operand's row lives in registers), N up to 4096
-// (small operand staged in smem), outputs streamed n by n with lanes along v.
-template <int KMAX>
+// (small operand staged in smem as [N][Kp], Kp = even K, read as 16-B pairs of k),
+// outputs streamed n by n with lanes along v; VEC = 2 as in the skinny kernel.
+template <int KMAX, int VEC>
 __global__ void __launch_bounds__(256) einsum_wide_kernel(const EinsumDesc* __restrict__ gd,
                                                           const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) EinsumDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
-  const int K = (int)d.K, N = (int)d.N;
-  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [N][K]
+  const int K = (int)d.K, N = (int)d.N, Kp = (K + 1) & ~1;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [N][Kp]
   const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
   const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
-  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
-    const int n = e / K, k = e % K;
-    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  for (int e = threadIdx.x; e < Kp * N; e += blockDim.x) {
+    const int n = e / Kp, k = e % Kp;
+    Bs[e] = k < K ? B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)]
+                  : make_float2(0.f, 0.f);
   }
   __syncthreads();
-  const int64_t V = d.V;
+  const int64_t V = d.V, Vv = V / VEC, Mv = d.M / VEC;
   const int64_t vstride = d.m_sa[d.nm - 1];
   float amax = 0.f;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < d.M;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mv;
        m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = m % V, o = m / V;
+    const int64_t vi = (m % Vv) * VEC, o = m / Vv;
     const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
-    float2 a[KMAX];
+    float2 a[KMAX][VEC];
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-      a[k] = k < K ? a_row[decompose(k, d.nk, d.k_ext, d.k_sa)] : make_float2(0.f, 0.f);
+    for (int k = 0; k < KMAX; ++k) {
+      if (k < K) {
+        const float2* p = a_row + decompose(k, d.nk, d.k_ext, d.k_sa);
+        if (VEC == 2) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+          a[k][0] = make_float2(q.x, q.y);
+          a[k][VEC - 1] = make_float2(q.z, q.w);
+        } else {
+          a[k][0] = __ldg(p);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) a[k][u] = make_float2(0.f, 0.f);
+      }
+    }
+    float2* crow = d.C + o * N * V + vi;
     for (int n = 0; n < N; ++n) {
-      float cr = 0.f, ci = 0.f;
+      float cr[VEC], ci[VEC];
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        if (k < K) {
-          const float2 b = Bs[n * K + k];
-          cr = fmaf(a[k].x, b.x, cr);
-          cr = fmaf(-a[k].y, b.y, cr);
-          ci = fmaf(a[k].x, b.y, ci);
-          ci = fmaf(a[k].y, b.x, ci);
+      for (int u = 0; u < VEC; ++u) { cr[u] = 0.f; ci[u] = 0.f; }
+      const float4* brow = reinterpret_cast<const float4*>(Bs + n * Kp);
+#pragma unroll
+      for (int k2 = 0; k2 < KMAX / 2; ++k2) {
+        if (2 * k2 < K) {
+          const float4 b = brow[k2];         // B[n][2k2] = (x, y), B[n][2k2+1] = (z, w)
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) {
+            const float2 x0 = a[2 * k2][u], x1 = a[2 * k2 + 1][u];
+            cr[u] = fmaf(x0.x, b.x, fmaf(-x0.y, b.y, fmaf(x1.x, b.z, fmaf(-x1.y, b.w, cr[u]))));
+            ci[u] = fmaf(x0.x, b.y, fmaf(x0.y, b.x, fmaf(x1.x, b.w, fmaf(x1.y, b.z, ci[u]))));
+          }
         }
       }
-      store_out(d, (o * N + n) * V + vi, cr, ci, amax);
+      if (VEC == 2 && !d.acc) {
+        *reinterpret_cast<float4*>(crow + (int64_t)n * V) = make_float4(cr[0], ci[0], cr[VEC - 1], ci[VEC - 1]);
+        amax = fmaxf(amax, fmaxf(fmaxf(fabsf(cr[0]), fabsf(ci[0])), fmaxf(fabsf(cr[VEC - 1]), fabsf(ci[VEC - 1]))));
+      } else {
+#pragma unroll
+        for (int u = 0; u < VEC; ++u)
+          store_out_f(d, (o * N + n) * V + vi + u, cr[u], ci[u], amax);
+      }
     }
   }
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
@@ -815,36 +804,53 @@ bool tn_vec2_enabled() {   // TN_SKINNY_VEC2=0 disables the paired-lane kernel (
 template <typename F>
 cudaError_t allow_big_smem(F* kern) {
   // the staged small operand can exceed the 48 KB default dynamic smem window
-  static_assert(sizeof(F*) > 0, "");
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+}
+
+template <int NMAX>
+cudaError_t enable_skinny(cudaError_t e) {
+  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, false>);
+  if constexpr (NMAX <= 16) {
+    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, true>);
+    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, false>);
+  }
+  return e;
+}
+
+template <int KMAX>
+cudaError_t enable_wide(cudaError_t e) {
+  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 1>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 2>);
+  return e;
 }
 
 cudaError_t enable_einsum_smem() {
   static bool done = false;
   if (done) return cudaSuccess;
-  cudaError_t e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<4, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<8, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<16, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<32, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<64, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<4, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<8, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<16, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<32, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny_kernel<64, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny2_kernel<4, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny2_kernel<8, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny2_kernel<16, true>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny2_kernel<4, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny2_kernel<8, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_skinny2_kernel<16, false>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_wide_kernel<2>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_wide_kernel<4>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_wide_kernel<8>)) != cudaSuccess) return e;
-  if ((e = allow_big_smem(einsum_wide_kernel<16>)) != cudaSuccess) return e;
-  done = true;
-  return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  e = enable_skinny<4>(e); e = enable_skinny<8>(e); e = enable_skinny<16>(e);
+  e = enable_skinny<32>(e); e = enable_skinny<64>(e);
+  e = enable_wide<2>(e); e = enable_wide<4>(e); e = enable_wide<8>(e); e = enable_wide<16>(e);
+  if (e == cudaSuccess) done = true;
+  return e;
+}
+
+template <int NMAX, int VEC>
+void launch_skinny(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
+                   cudaStream_t s) {
+  if constexpr (VEC == 1 || NMAX <= 16) {   // paired lanes only up to N = 16 (registers)
+    const int g = grid_for(h.M / VEC, 256);
+    if (h.pow2) einsum_skinny_kernel<NMAX, VEC, true><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    else einsum_skinny_kernel<NMAX, VEC, false><<<g, 256, smem, s>>>(d_desc, leaf_off);
+  }
+}
+
+template <int KMAX>
+void launch_wide(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
+                 bool vec2, cudaStream_t s) {
+  if (vec2) einsum_wide_kernel<KMAX, 2><<<grid_for(h.M / 2, 256), 256, smem, s>>>(d_desc, leaf_off);
+  else einsum_wide_kernel<KMAX, 1><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
 }
 
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off,
@@ -854,18 +860,16 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     cudaError_t e = enable_einsum_smem();
     if (e != cudaSuccess) return e;
   }
+  // pairs of lanes (16-B accesses) when the lane run is unit-stride and even and the
+  // big operand's base is 16-B aligned (a leaf's dynamic slice offset is a sum of
+  // strides of power-of-two dims above the unit-stride one, hence even)
+  const bool vec2 = h.pow2 && h.m_sa[h.nm - 1] == 1 && h.V % 2 == 0 && h.a_off % 2 == 0 &&
+                    tn_vec2_enabled();
   if (h.mode == 1) {
-    const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
-    const int g = grid_for(h.M, th);
-    // pairs of lanes (16-B accesses) when the lane run is unit-stride, even and the
-    // big operand is an aligned intermediate (never a leaf with a slice offset)
-    const bool vec2 = h.pow2 && h.m_sa[h.nm - 1] == 1 && h.V % 2 == 0 && h.a_leaf < 0 &&
-                      h.a_off % 2 == 0 && h.N <= 16 && tn_vec2_enabled();
-#define TN_SKINNY(NM)                                                                     \
-  (vec2 ? (h.pow2 ? einsum_skinny2_kernel<NM, true><<<grid_for(h.M / 2, th), th, smem, s>>>(d_desc, leaf_off) \
-                  : einsum_skinny2_kernel<NM, false><<<grid_for(h.M / 2, th), th, smem, s>>>(d_desc, leaf_off)) \
-        : (h.pow2 ? einsum_skinny_kernel<NM, true><<<g, th, smem, s>>>(d_desc, leaf_off)  \
-                  : einsum_skinny_kernel<NM, false><<<g, th, smem, s>>>(d_desc, leaf_off)))
+    const size_t smem = sizeof(float2) * h.K * ((h.N + 1) & ~1) + sizeof(int64_t) * h.K;
+#define TN_SKINNY(NM)                                                            \
+  (vec2 && NM <= 16 ? launch_skinny<NM, 2>(d_desc, h, leaf_off, smem, s)         \
+                    : launch_skinny<NM, 1>(d_desc, h, leaf_off, smem, s))
     if (h.N <= 4) TN_SKINNY(4);
     else if (h.N <= 8) TN_SKINNY(8);
     else if (h.N <= 16) TN_SKINNY(16);
@@ -875,12 +879,11 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     return cudaGetLastError();
   }
   if (h.mode == 3) {
-    const size_t smem = sizeof(float2) * h.K * h.N;
-    const int g = grid_for(h.M, th);
-    if (h.K <= 2) einsum_wide_kernel<2><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else if (h.K <= 4) einsum_wide_kernel<4><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else if (h.K <= 8) einsum_wide_kernel<8><<<g, th, smem, s>>>(d_desc, leaf_off);
-    else einsum_wide_kernel<16><<<g, th, smem, s>>>(d_desc, leaf_off);
+    const size_t smem = sizeof(float2) * ((h.K + 1) & ~1) * h.N;
+    if (h.K <= 2) launch_wide<2>(d_desc, h, leaf_off, smem, vec2, s);
+    else if (h.K <= 4) launch_wide<4>(d_desc, h, leaf_off, smem, vec2, s);
+    else if (h.K <= 8) launch_wide<8>(d_desc, h, leaf_off, smem, vec2, s);
+    else launch_wide<16>(d_desc, h, leaf_off, smem, vec2, s);
     return cudaGetLastError();
   }
   if (h.mode == 2) {
