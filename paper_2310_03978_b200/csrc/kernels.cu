@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
 // loop issues KU loads before any use (memory-level parallelism), and B is read
 // as 16-B pairs of n, so one shared-memory load feeds 8·VEC FMAs.  fp32
 // accumulation (K <= 256 here).
-template <int NMAX, int VEC, bool POW2>
+template <int NMAX, int VEC, bool POW2, int KP>
 __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __restrict__ gd,
                                                             const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) EinsumDesc d;
@@ -534,6 +534,19 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
       for (int n = 0; n < NMAX; ++n) { cr[u][n] = 0.f; ci[u][n] = 0.f; }
     for (int k0 = 0; k0 < K; k0 += KU) {
       float2 a[KU][VEC];
+      if (KP == 2) {       // (k, k+1) adjacent in A (innermost k dim unit-stride): 16-B loads
+#pragma unroll
+        for (int kk = 0; kk < KU; kk += 2) {
+          if (k0 + kk < K) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(a_row + koff[k0 + kk]));
+            a[kk][0] = make_float2(q.x, q.y);
+            a[kk + 1][0] = make_float2(q.z, q.w);
+          } else {
+            a[kk][0] = make_float2(0.f, 0.f);
+            a[kk + 1][0] = make_float2(0.f, 0.f);
+          }
+        }
+      } else
 #pragma unroll
       for (int kk = 0; kk < KU; ++kk) {
         if (k0 + kk < K) {
@@ -594,7 +607,7 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
 // like steps: K <= KMAX (the big operand's row lives in registers), N up to 4096
 // (small operand staged in smem as [N][Kp], Kp = even K, read as 16-B pairs of k),
 // outputs streamed n by n with lanes along v; VEC = 2 as in the skinny kernel.
-template <int KMAX, int VEC>
+template <int KMAX, int VEC, int KP>
 __global__ void __launch_bounds__(256) einsum_wide_kernel(const EinsumDesc* __restrict__ gd,
                                                           const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) EinsumDesc d;
@@ -618,6 +631,19 @@ __global__ void __launch_bounds__(256) einsum_wide_kernel(const EinsumDesc* __re
     const int64_t vi = (m % Vv) * VEC, o = m / Vv;
     const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
     float2 a[KMAX][VEC];
+    if (KP == 2) {         // (k, k+1) adjacent in A: 16-B loads
+#pragma unroll
+      for (int k = 0; k < KMAX; k += 2) {
+        if (k < K) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(a_row + decompose(k, d.nk, d.k_ext, d.k_sa)));
+          a[k][0] = make_float2(q.x, q.y);
+          a[k + 1][0] = make_float2(q.z, q.w);
+        } else {
+          a[k][0] = make_float2(0.f, 0.f);
+          a[k + 1][0] = make_float2(0.f, 0.f);
+        }
+      }
+    } else
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
       if (k < K) {
@@ -809,19 +835,21 @@ cudaError_t allow_big_smem(F* kern) {
 
 template <int NMAX>
 cudaError_t enable_skinny(cudaError_t e) {
-  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true>);
-  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, false>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true, 1>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, false, 1>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true, 2>);
   if constexpr (NMAX <= 16) {
-    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, true>);
-    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, false>);
+    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, true, 1>);
+    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, false, 1>);
   }
   return e;
 }
 
 template <int KMAX>
 cudaError_t enable_wide(cudaError_t e) {
-  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 1>);
-  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 2>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 1, 1>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 2, 1>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_wide_kernel<KMAX, 1, 2>);
   return e;
 }
 
@@ -838,19 +866,21 @@ cudaError_t enable_einsum_smem() {
 
 template <int NMAX, int VEC>
 void launch_skinny(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
-                   cudaStream_t s) {
+                   bool kpair, cudaStream_t s) {
   if constexpr (VEC == 1 || NMAX <= 16) {   // paired lanes only up to N = 16 (registers)
     const int g = grid_for(h.M / VEC, 256);
-    if (h.pow2) einsum_skinny_kernel<NMAX, VEC, true><<<g, 256, smem, s>>>(d_desc, leaf_off);
-    else einsum_skinny_kernel<NMAX, VEC, false><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    if (VEC == 1 && kpair) einsum_skinny_kernel<NMAX, 1, true, 2><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    else if (h.pow2) einsum_skinny_kernel<NMAX, VEC, true, 1><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    else einsum_skinny_kernel<NMAX, VEC, false, 1><<<g, 256, smem, s>>>(d_desc, leaf_off);
   }
 }
 
 template <int KMAX>
 void launch_wide(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
-                 bool vec2, cudaStream_t s) {
-  if (vec2) einsum_wide_kernel<KMAX, 2><<<grid_for(h.M / 2, 256), 256, smem, s>>>(d_desc, leaf_off);
-  else einsum_wide_kernel<KMAX, 1><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
+                 bool vec2, bool kpair, cudaStream_t s) {
+  if (vec2) einsum_wide_kernel<KMAX, 2, 1><<<grid_for(h.M / 2, 256), 256, smem, s>>>(d_desc, leaf_off);
+  else if (kpair) einsum_wide_kernel<KMAX, 1, 2><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
+  else einsum_wide_kernel<KMAX, 1, 1><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
 }
 
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off,
@@ -865,11 +895,17 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
   // strides of power-of-two dims above the unit-stride one, hence even)
   const bool vec2 = h.pow2 && h.m_sa[h.nm - 1] == 1 && h.V % 2 == 0 && h.a_off % 2 == 0 &&
                     tn_vec2_enabled();
+  // pairs of k (16-B loads along a row of A) when A's innermost k dim is unit-stride
+  // with an even extent and every other stride of A is even
+  bool kpair = h.pow2 && h.nk > 0 && h.k_sa[h.nk - 1] == 1 && h.k_ext[h.nk - 1] % 2 == 0 &&
+               h.K % 2 == 0 && h.a_off % 2 == 0 && tn_vec2_enabled();
+  for (int i = 0; i < h.nm && kpair; ++i) kpair = h.m_sa[i] % 2 == 0 || h.m_ext[i] == 1;
+  for (int i = 0; i + 1 < h.nk && kpair; ++i) kpair = h.k_sa[i] % 2 == 0;
   if (h.mode == 1) {
     const size_t smem = sizeof(float2) * h.K * ((h.N + 1) & ~1) + sizeof(int64_t) * h.K;
 #define TN_SKINNY(NM)                                                            \
-  (vec2 && NM <= 16 ? launch_skinny<NM, 2>(d_desc, h, leaf_off, smem, s)         \
-                    : launch_skinny<NM, 1>(d_desc, h, leaf_off, smem, s))
+  (vec2 && NM <= 16 ? launch_skinny<NM, 2>(d_desc, h, leaf_off, smem, false, s)  \
+                    : launch_skinny<NM, 1>(d_desc, h, leaf_off, smem, kpair, s))
     if (h.N <= 4) TN_SKINNY(4);
     else if (h.N <= 8) TN_SKINNY(8);
     else if (h.N <= 16) TN_SKINNY(16);
@@ -880,10 +916,10 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
   }
   if (h.mode == 3) {
     const size_t smem = sizeof(float2) * ((h.K + 1) & ~1) * h.N;
-    if (h.K <= 2) launch_wide<2>(d_desc, h, leaf_off, smem, vec2, s);
-    else if (h.K <= 4) launch_wide<4>(d_desc, h, leaf_off, smem, vec2, s);
-    else if (h.K <= 8) launch_wide<8>(d_desc, h, leaf_off, smem, vec2, s);
-    else launch_wide<16>(d_desc, h, leaf_off, smem, vec2, s);
+    if (h.K <= 2) launch_wide<2>(d_desc, h, leaf_off, smem, vec2, kpair, s);
+    else if (h.K <= 4) launch_wide<4>(d_desc, h, leaf_off, smem, vec2, kpair, s);
+    else if (h.K <= 8) launch_wide<8>(d_desc, h, leaf_off, smem, vec2, kpair, s);
+    else launch_wide<16>(d_desc, h, leaf_off, smem, vec2, kpair, s);
     return cudaGetLastError();
   }
   if (h.mode == 2) {

@@ -1146,6 +1146,15 @@ tn_status build_plan(tn_ctx* c) {
       e.acc = sp.final_step ? c->d_acc : nullptr;
       fill_shifts(e);
       sp.hdesc = e;
+      if (c->debug_plan) {
+        fprintf(stderr, "[tn] step %d simt mode %d M=%lld N=%lld K=%lld V=%lld vstride=%lld a_off%%2=%lld leaf=%d pow2=%d x:", s,
+                e.mode, (long long)e.M, (long long)e.N, (long long)e.K, (long long)e.V,
+                (long long)e.m_sa[e.nm - 1], (long long)(e.a_off % 2), e.a_leaf, e.pow2);
+        for (int d = 0; d < e.nm; ++d) fprintf(stderr, " %lldx%lld", (long long)e.m_ext[d], (long long)e.m_sa[d]);
+        fprintf(stderr, " | k:");
+        for (int d = 0; d < e.nk; ++d) fprintf(stderr, " %lldx%lld", (long long)e.k_ext[d], (long long)e.k_sa[d]);
+        fprintf(stderr, "\n");
+      }
     } else if (!sp.tc) {
       tn::EinsumDesc& e = eds[sp.einsum_idx];
       memset(&e, 0, sizeof(e));

@@ -8,3 +8,6 @@ timeout 600 python bench.py --steps 5 --warmup 3 --precision mixed --no-cpu-base
 python -c "import json; d=json.load(open('gpurun_out/bench_mixed.json')); print('MIX', d['value'], d['ms_per_step'], d['roofline']['achieved'])"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_bench.log 2>&1; echo ncu1_rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cgemm -s ${TOPGEMM:-27} -c 1 -o gpurun_out/prof_gemm_top python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1; echo ncu2_rc=$?
+rm -f gpurun_out/group.jsonl
+for g in 4 8 16; do TN_GEMM_GROUP=$g timeout 120 python tools/gemm_bench.py 32768 16384 16384 --out gpurun_out/group.jsonl > /dev/null 2>&1; done
+cut -c1-160 gpurun_out/group.jsonl
