@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(256) einsum_kernel(const EinsumDesc* __restric
 // loop issues KU loads before any use (memory-level parallelism), and B is read
 // as 16-B pairs of n, so one shared-memory load feeds 8·VEC FMAs.  fp32
 // accumulation (K <= 256 here).
-template <int NMAX, int VEC, bool POW2, int KP>
+template <int NMAX, int VEC, bool POW2, int KP, int R>
 __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __restrict__ gd,
                                                             const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) EinsumDesc d;
@@ -518,48 +518,66 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
   __syncthreads();
-  constexpr int KU = NMAX <= 16 ? 8 : 4;
+  // k values loaded per row before any use; R rows per thread (grid-stride apart, so
+  // every warp access stays lane-coalesced): R·KU·VEC·8 B in flight per thread
+  constexpr int KU = R == 4 ? 4 : (R == 2 ? (VEC == 2 ? 4 : 8) : (NMAX <= 16 ? 8 : 4));
   const int64_t V = d.V, Vv = V / VEC, Mv = d.M / VEC;
   const int64_t vstride = d.m_sa[d.nm - 1];
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
   float amax = 0.f;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mv;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = (m % Vv) * VEC, o = m / Vv;
-    const float2* a_row = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
-                                    : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
-    float cr[VEC][NMAX], ci[VEC][NMAX];
+  for (int64_t m0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m0 < Mv; m0 += R * step) {
+    const float2* a_row[R];
+    int64_t obase[R];
+    bool live[R];
 #pragma unroll
-    for (int u = 0; u < VEC; ++u)
+    for (int r = 0; r < R; ++r) {
+      const int64_t m = m0 + r * step;
+      live[r] = m < Mv;
+      const int64_t mm = live[r] ? m : m0;
+      const int64_t vi = (mm % Vv) * VEC, o = mm / Vv;
+      a_row[r] = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
+                           : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
+      obase[r] = o * N * V + vi;
+    }
+    float cr[R][VEC][NMAX], ci[R][VEC][NMAX];
 #pragma unroll
-      for (int n = 0; n < NMAX; ++n) { cr[u][n] = 0.f; ci[u][n] = 0.f; }
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int u = 0; u < VEC; ++u)
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) { cr[r][u][n] = 0.f; ci[r][u][n] = 0.f; }
     for (int k0 = 0; k0 < K; k0 += KU) {
-      float2 a[KU][VEC];
-      if (KP == 2) {       // (k, k+1) adjacent in A (innermost k dim unit-stride): 16-B loads
+      float2 a[KU][R][VEC];
 #pragma unroll
-        for (int kk = 0; kk < KU; kk += 2) {
-          if (k0 + kk < K) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(a_row + koff[k0 + kk]));
-            a[kk][0] = make_float2(q.x, q.y);
-            a[kk + 1][0] = make_float2(q.z, q.w);
-          } else {
-            a[kk][0] = make_float2(0.f, 0.f);
-            a[kk + 1][0] = make_float2(0.f, 0.f);
-          }
-        }
-      } else
+      for (int r = 0; r < R; ++r) {
+        if (KP == 2) {     // (k, k+1) adjacent in A (innermost k dim unit-stride): 16-B loads
 #pragma unroll
-      for (int kk = 0; kk < KU; ++kk) {
-        if (k0 + kk < K) {
-          if (VEC == 2) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(a_row + koff[k0 + kk]));
-            a[kk][0] = make_float2(q.x, q.y);
-            a[kk][VEC - 1] = make_float2(q.z, q.w);
-          } else {
-            a[kk][0] = __ldg(a_row + koff[k0 + kk]);
+          for (int kk = 0; kk < KU; kk += 2) {
+            if (k0 + kk < K) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(a_row[r] + koff[k0 + kk]));
+              a[kk][r][0] = make_float2(q.x, q.y);
+              a[kk + 1][r][0] = make_float2(q.z, q.w);
+            } else {
+              a[kk][r][0] = make_float2(0.f, 0.f);
+              a[kk + 1][r][0] = make_float2(0.f, 0.f);
+            }
           }
         } else {
 #pragma unroll
-          for (int u = 0; u < VEC; ++u) a[kk][u] = make_float2(0.f, 0.f);
+          for (int kk = 0; kk < KU; ++kk) {
+            if (k0 + kk < K) {
+              if (VEC == 2) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(a_row[r] + koff[k0 + kk]));
+                a[kk][r][0] = make_float2(q.x, q.y);
+                a[kk][r][VEC - 1] = make_float2(q.z, q.w);
+              } else {
+                a[kk][r][0] = __ldg(a_row[r] + koff[k0 + kk]);
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < VEC; ++u) a[kk][r][u] = make_float2(0.f, 0.f);
+            }
+          }
         }
       }
 #pragma unroll
@@ -571,30 +589,36 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
             if (2 * n2 < N) {
               const float4 b = brow[n2];     // B[2n2] = (x, y), B[2n2+1] = (z, w)
 #pragma unroll
-              for (int u = 0; u < VEC; ++u) {
-                const float2 x = a[kk][u];
-                cr[u][2 * n2] = fmaf(x.x, b.x, fmaf(-x.y, b.y, cr[u][2 * n2]));
-                ci[u][2 * n2] = fmaf(x.x, b.y, fmaf(x.y, b.x, ci[u][2 * n2]));
-                cr[u][2 * n2 + 1] = fmaf(x.x, b.z, fmaf(-x.y, b.w, cr[u][2 * n2 + 1]));
-                ci[u][2 * n2 + 1] = fmaf(x.x, b.w, fmaf(x.y, b.z, ci[u][2 * n2 + 1]));
-              }
+              for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int u = 0; u < VEC; ++u) {
+                  const float2 x = a[kk][r][u];
+                  cr[r][u][2 * n2] = fmaf(x.x, b.x, fmaf(-x.y, b.y, cr[r][u][2 * n2]));
+                  ci[r][u][2 * n2] = fmaf(x.x, b.y, fmaf(x.y, b.x, ci[r][u][2 * n2]));
+                  cr[r][u][2 * n2 + 1] = fmaf(x.x, b.z, fmaf(-x.y, b.w, cr[r][u][2 * n2 + 1]));
+                  ci[r][u][2 * n2 + 1] = fmaf(x.x, b.w, fmaf(x.y, b.z, ci[r][u][2 * n2 + 1]));
+                }
             }
           }
         }
       }
     }
-    const int64_t base = o * N * V + vi;
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      if (n < N) {
-        const int64_t idx = base + (int64_t)n * V;
-        if (VEC == 2 && !d.acc) {
-          *reinterpret_cast<float4*>(d.C + idx) = make_float4(cr[0][n], ci[0][n], cr[VEC - 1][n], ci[VEC - 1][n]);
-          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(cr[0][n]), fabsf(ci[0][n])),
-                                   fmaxf(fabsf(cr[VEC - 1][n]), fabsf(ci[VEC - 1][n]))));
-        } else {
+    for (int r = 0; r < R; ++r) {
+      if (!live[r]) continue;
 #pragma unroll
-          for (int u = 0; u < VEC; ++u) store_out_f(d, idx + u, cr[u][n], ci[u][n], amax);
+      for (int n = 0; n < NMAX; ++n) {
+        if (n < N) {
+          const int64_t idx = obase[r] + (int64_t)n * V;
+          if (VEC == 2 && !d.acc) {
+            *reinterpret_cast<float4*>(d.C + idx) =
+                make_float4(cr[r][0][n], ci[r][0][n], cr[r][VEC - 1][n], ci[r][VEC - 1][n]);
+            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(cr[r][0][n]), fabsf(ci[r][0][n])),
+                                     fmaxf(fabsf(cr[r][VEC - 1][n]), fabsf(ci[r][VEC - 1][n]))));
+          } else {
+#pragma unroll
+            for (int u = 0; u < VEC; ++u) store_out_f(d, idx + u, cr[r][u][n], ci[r][u][n], amax);
+          }
         }
       }
     }
@@ -686,6 +710,192 @@ __global__ void __launch_bounds__(256) einsum_wide_kernel(const EinsumDesc* __re
         for (int u = 0; u < VEC; ++u)
           store_out_f(d, (o * N + n) * V + vi + u, cr[u], ci[u], amax);
       }
+    }
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+// ---------------------------------------------------------------- SIMT einsum, skinny (previous design, TN_SIMT_OLD=1 A/B)
+// C[o][n][v] = Σ_k A[o, v, k] B[n, k] for a small B (N*K <= 8192 complex, staged
+// in smem once per block) and a big A streamed exactly once: lanes walk A's
+// smallest-stride free dim v (coalesced reads), the output keeps v innermost
+// (coalesced writes).  These are the HBM-bound "absorb a gate into the stem"
+// steps (stage 1 dominates).  fp32 accumulation (K <= 64 here).
+template <int NMAX, bool POW2>
+__global__ void __launch_bounds__(256) einsum_skinny_old_kernel(const EinsumDesc* __restrict__ gd,
+                                                            const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int K = (int)d.K, N = (int)d.N;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][N]
+  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * N);
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int k = e / N, n = e % N;
+    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
+  __syncthreads();
+  const int64_t V = d.V;
+  const int64_t vstride = d.m_sa[d.nm - 1];
+  // U rows per thread per iteration (independent loads in flight); U = 2 while
+  // the accumulators fit comfortably in registers
+  constexpr int U = NMAX <= 16 ? 2 : 1;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  float amax = 0.f;
+  for (int64_t m0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m0 < d.M; m0 += U * step) {
+    const float2* a_row[U];
+    int64_t obase[U];
+    bool live[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t m = m0 + u * step;
+      live[u] = m < d.M;
+      const int64_t mm = live[u] ? m : m0;
+      const int64_t vi = mm % V, o = mm / V;
+      a_row[u] = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
+                           : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
+      obase[u] = o * N * V + vi;
+    }
+    float accr[U][NMAX], acci[U][NMAX];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) { accr[u][n] = 0.f; acci[u][n] = 0.f; }
+    for (int k = 0; k < K; ++k) {
+      float2 a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = a_row[u][koff[k]];
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n < N) {
+          const float2 b = Bs[k * N + n];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            accr[u][n] = fmaf(a[u].x, b.x, accr[u][n]);
+            accr[u][n] = fmaf(-a[u].y, b.y, accr[u][n]);
+            acci[u][n] = fmaf(a[u].x, b.y, acci[u][n]);
+            acci[u][n] = fmaf(a[u].y, b.x, acci[u][n]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (live[u])
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+          if (n < N) store_out_f(d, obase[u] + (int64_t)n * V, accr[u][n], acci[u][n], amax);
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+// Vectorised variant: the lane run v is unit-stride and even, so a thread owns the
+// pair (v, v+1): one 16-byte load per k and one 16-byte store per n (pairs are
+// adjacent in A and in C), half the instructions per byte of the scalar kernel.
+template <int NMAX, bool POW2>
+__global__ void __launch_bounds__(256) einsum_skinny2_old_kernel(const EinsumDesc* __restrict__ gd,
+                                                             const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int K = (int)d.K, N = (int)d.N;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][N]
+  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * N);
+  const float2* A = d.A + d.a_off;
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int k = e / N, n = e % N;
+    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
+  __syncthreads();
+  const int64_t V = d.V, Vh = V / 2, Mh = d.M / 2;
+  float amax = 0.f;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mh;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t vi = (m % Vh) * 2, o = m / Vh;
+    const float2* a_row = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
+                                    : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi;
+    float r0[NMAX], i0[NMAX], r1[NMAX], i1[NMAX];
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) { r0[n] = 0.f; i0[n] = 0.f; r1[n] = 0.f; i1[n] = 0.f; }
+    for (int k = 0; k < K; ++k) {
+      const float4 q = *reinterpret_cast<const float4*>(a_row + koff[k]);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n < N) {
+          const float2 b = Bs[k * N + n];
+          r0[n] = fmaf(q.x, b.x, r0[n]); r0[n] = fmaf(-q.y, b.y, r0[n]);
+          i0[n] = fmaf(q.x, b.y, i0[n]); i0[n] = fmaf(q.y, b.x, i0[n]);
+          r1[n] = fmaf(q.z, b.x, r1[n]); r1[n] = fmaf(-q.w, b.y, r1[n]);
+          i1[n] = fmaf(q.z, b.y, i1[n]); i1[n] = fmaf(q.w, b.x, i1[n]);
+        }
+      }
+    }
+    const int64_t base = o * N * V + vi;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n < N) {
+        const int64_t idx = base + (int64_t)n * V;
+        if (d.acc) {
+          store_out_f(d, idx, r0[n], i0[n], amax);
+          store_out_f(d, idx + 1, r1[n], i1[n], amax);
+        } else {
+          *reinterpret_cast<float4*>(d.C + idx) = make_float4(r0[n], i0[n], r1[n], i1[n]);
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0[n]), fabsf(i0[n])), fmaxf(fabsf(r1[n]), fabsf(i1[n]))));
+        }
+      }
+    }
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
+// ---------------------------------------------------------------- SIMT einsum, wide skinny
+// Same layout contract as einsum_skinny_old_kernel (out [Mo][N][V]) for outer-product-
+// like steps: K <= KMAX (the big operand's row lives in registers), N up to 4096
+// (small operand staged in smem), outputs streamed n by n with lanes along v.
+template <int KMAX>
+__global__ void __launch_bounds__(256) einsum_wide_old_kernel(const EinsumDesc* __restrict__ gd,
+                                                          const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int K = (int)d.K, N = (int)d.N;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [N][K]
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int n = e / K, k = e % K;
+    Bs[e] = B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)];
+  }
+  __syncthreads();
+  const int64_t V = d.V;
+  const int64_t vstride = d.m_sa[d.nm - 1];
+  float amax = 0.f;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < d.M;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t vi = m % V, o = m / V;
+    const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
+    float2 a[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      a[k] = k < K ? a_row[decompose(k, d.nk, d.k_ext, d.k_sa)] : make_float2(0.f, 0.f);
+    for (int n = 0; n < N; ++n) {
+      float cr = 0.f, ci = 0.f;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k < K) {
+          const float2 b = Bs[n * K + k];
+          cr = fmaf(a[k].x, b.x, cr);
+          cr = fmaf(-a[k].y, b.y, cr);
+          ci = fmaf(a[k].x, b.y, ci);
+          ci = fmaf(a[k].y, b.x, ci);
+        }
+      }
+      store_out(d, (o * N + n) * V + vi, cr, ci, amax);
     }
   }
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
@@ -833,14 +1043,25 @@ cudaError_t allow_big_smem(F* kern) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
 }
 
+// instantiated (NMAX, VEC, R) combinations keep the accumulators in registers
+template <int NMAX, int VEC, int R>
+constexpr bool skinny_ok() { return NMAX * VEC * R <= 32 || R == 1; }
+
+template <int NMAX, int VEC, int R>
+cudaError_t enable_skinny_r(cudaError_t e) {
+  if constexpr (skinny_ok<NMAX, VEC, R>()) {
+    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, VEC, true, 1, R>);
+    if (VEC == 1 && e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true, 2, R>);
+  }
+  return e;
+}
+
 template <int NMAX>
 cudaError_t enable_skinny(cudaError_t e) {
-  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true, 1>);
-  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, false, 1>);
-  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, true, 2>);
+  if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 1, false, 1, 1>);
+  e = enable_skinny_r<NMAX, 1, 1>(e); e = enable_skinny_r<NMAX, 1, 2>(e); e = enable_skinny_r<NMAX, 1, 4>(e);
   if constexpr (NMAX <= 16) {
-    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, true, 1>);
-    if (e == cudaSuccess) e = allow_big_smem(einsum_skinny_kernel<NMAX, 2, false, 1>);
+    e = enable_skinny_r<NMAX, 2, 1>(e); e = enable_skinny_r<NMAX, 2, 2>(e);
   }
   return e;
 }
@@ -864,14 +1085,35 @@ cudaError_t enable_einsum_smem() {
   return e;
 }
 
+template <int NMAX, int VEC, int R>
+bool launch_skinny_r(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
+                     bool kpair, cudaStream_t s) {
+  if constexpr (skinny_ok<NMAX, VEC, R>()) {
+    const int g = grid_for((h.M / VEC + R - 1) / R, 256);
+    if (VEC == 1 && kpair) einsum_skinny_kernel<NMAX, 1, true, 2, R><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    else einsum_skinny_kernel<NMAX, VEC, true, 1, R><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    return true;
+  }
+  return false;
+}
+
+// rows per thread: enough that one round of loads is >= 16 complex (128 B) in flight
 template <int NMAX, int VEC>
 void launch_skinny(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
-                   bool kpair, cudaStream_t s) {
+                   bool kpair, int rows, cudaStream_t s) {
   if constexpr (VEC == 1 || NMAX <= 16) {   // paired lanes only up to N = 16 (registers)
-    const int g = grid_for(h.M / VEC, 256);
-    if (VEC == 1 && kpair) einsum_skinny_kernel<NMAX, 1, true, 2><<<g, 256, smem, s>>>(d_desc, leaf_off);
-    else if (h.pow2) einsum_skinny_kernel<NMAX, VEC, true, 1><<<g, 256, smem, s>>>(d_desc, leaf_off);
-    else einsum_skinny_kernel<NMAX, VEC, false, 1><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    if (!h.pow2) {
+      einsum_skinny_kernel<NMAX, VEC, false, 1, 1><<<grid_for(h.M / VEC, 256), 256, smem, s>>>(d_desc, leaf_off);
+      return;
+    }
+    static const int rforce = getenv("TN_SKINNY_ROWS") ? atoi(getenv("TN_SKINNY_ROWS")) : 0;
+    const int64_t kl = h.K < 8 ? h.K : 8;
+    int R = (int)std::max<int64_t>(1, std::min<int64_t>(4, 16 / (kl * VEC)));
+    if (rows) R = rows;
+    if (rforce) R = rforce;
+    if (R >= 4 && launch_skinny_r<NMAX, VEC, 4>(d_desc, h, leaf_off, smem, kpair, s)) return;
+    if (R >= 2 && launch_skinny_r<NMAX, VEC, 2>(d_desc, h, leaf_off, smem, kpair, s)) return;
+    launch_skinny_r<NMAX, VEC, 1>(d_desc, h, leaf_off, smem, kpair, s);
   }
 }
 
@@ -883,8 +1125,14 @@ void launch_wide(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* l
   else einsum_wide_kernel<KMAX, 1, 1><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
 }
 
+int einsum_variants(const EinsumDesc& h) {
+  if (h.mode == 1) return 4;   // 0 heuristic rows, 1 previous design, 2..3: R = 1, 2 (new design)
+  if (h.mode == 3) return 2;   // 0 new design, 1 previous design
+  return 1;
+}
+
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off,
-                          cudaStream_t s) {
+                          cudaStream_t s, int variant) {
   const int th = 256;
   if (h.mode == 1 || h.mode == 3) {
     cudaError_t e = enable_einsum_smem();
@@ -901,11 +1149,48 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
                h.K % 2 == 0 && h.a_off % 2 == 0 && tn_vec2_enabled();
   for (int i = 0; i < h.nm && kpair; ++i) kpair = h.m_sa[i] % 2 == 0 || h.m_ext[i] == 1;
   for (int i = 0; i + 1 < h.nk && kpair; ++i) kpair = h.k_sa[i] % 2 == 0;
+  static const int simt_old = getenv("TN_SIMT_OLD") ? atoi(getenv("TN_SIMT_OLD")) : 0;
+  if ((simt_old || variant == 1) && (h.mode == 1 || h.mode == 3)) {
+    static bool attr = false;
+    if (!attr) {
+      allow_big_smem(einsum_skinny_old_kernel<4, true>); allow_big_smem(einsum_skinny_old_kernel<8, true>);
+      allow_big_smem(einsum_skinny_old_kernel<16, true>); allow_big_smem(einsum_skinny_old_kernel<32, true>);
+      allow_big_smem(einsum_skinny_old_kernel<64, true>); allow_big_smem(einsum_skinny_old_kernel<4, false>);
+      allow_big_smem(einsum_skinny_old_kernel<8, false>); allow_big_smem(einsum_skinny_old_kernel<16, false>);
+      allow_big_smem(einsum_skinny_old_kernel<32, false>); allow_big_smem(einsum_skinny_old_kernel<64, false>);
+      allow_big_smem(einsum_skinny2_old_kernel<4, true>); allow_big_smem(einsum_skinny2_old_kernel<8, true>);
+      allow_big_smem(einsum_skinny2_old_kernel<16, true>); allow_big_smem(einsum_wide_old_kernel<2>);
+      allow_big_smem(einsum_wide_old_kernel<4>); allow_big_smem(einsum_wide_old_kernel<8>);
+      allow_big_smem(einsum_wide_old_kernel<16>);
+      attr = true;
+    }
+    if (h.mode == 1) {
+      const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
+      const int g = grid_for(h.M, 256);
+      const bool v2 = h.pow2 && h.m_sa[h.nm - 1] == 1 && h.V % 2 == 0 && h.a_leaf < 0 && h.a_off % 2 == 0 && h.N <= 16;
+#define TN_SKO(NM) (v2 ? (void)(einsum_skinny2_old_kernel<NM, true><<<grid_for(h.M / 2, 256), 256, smem, s>>>(d_desc, leaf_off)) \
+                       : (void)(h.pow2 ? einsum_skinny_old_kernel<NM, true><<<g, 256, smem, s>>>(d_desc, leaf_off) \
+                                       : einsum_skinny_old_kernel<NM, false><<<g, 256, smem, s>>>(d_desc, leaf_off)))
+      if (h.N <= 4) TN_SKO(4); else if (h.N <= 8) TN_SKO(8); else if (h.N <= 16) TN_SKO(16);
+      else if (h.N <= 32) { h.pow2 ? einsum_skinny_old_kernel<32, true><<<g, 256, smem, s>>>(d_desc, leaf_off) : einsum_skinny_old_kernel<32, false><<<g, 256, smem, s>>>(d_desc, leaf_off); }
+      else { h.pow2 ? einsum_skinny_old_kernel<64, true><<<g, 256, smem, s>>>(d_desc, leaf_off) : einsum_skinny_old_kernel<64, false><<<g, 256, smem, s>>>(d_desc, leaf_off); }
+#undef TN_SKO
+    } else {
+      const size_t smem = sizeof(float2) * h.K * h.N;
+      const int g = grid_for(h.M, 256);
+      if (h.K <= 2) einsum_wide_old_kernel<2><<<g, 256, smem, s>>>(d_desc, leaf_off);
+      else if (h.K <= 4) einsum_wide_old_kernel<4><<<g, 256, smem, s>>>(d_desc, leaf_off);
+      else if (h.K <= 8) einsum_wide_old_kernel<8><<<g, 256, smem, s>>>(d_desc, leaf_off);
+      else einsum_wide_old_kernel<16><<<g, 256, smem, s>>>(d_desc, leaf_off);
+    }
+    return cudaGetLastError();
+  }
   if (h.mode == 1) {
+    const int rows = variant >= 2 ? variant - 1 : 0;
     const size_t smem = sizeof(float2) * h.K * ((h.N + 1) & ~1) + sizeof(int64_t) * h.K;
 #define TN_SKINNY(NM)                                                            \
-  (vec2 && NM <= 16 ? launch_skinny<NM, 2>(d_desc, h, leaf_off, smem, false, s)  \
-                    : launch_skinny<NM, 1>(d_desc, h, leaf_off, smem, kpair, s))
+  (vec2 && NM <= 16 ? launch_skinny<NM, 2>(d_desc, h, leaf_off, smem, false, rows, s)  \
+                    : launch_skinny<NM, 1>(d_desc, h, leaf_off, smem, kpair, rows, s))
     if (h.N <= 4) TN_SKINNY(4);
     else if (h.N <= 8) TN_SKINNY(8);
     else if (h.N <= 16) TN_SKINNY(16);

@@ -92,6 +92,7 @@ struct StepPlan {
   // order1) and column digits (Q dims, order2) with their strides in the output view
   bool out_gen = false;
   std::vector<VDim> po, qo;
+  int simt_variant = -1;        // SIMT kernel variant chosen by the first-slice autotuner
 };
 
 struct KStats {
@@ -116,6 +117,8 @@ struct tn_ctx {
   // k-blocks per promoted TMEM chunk: 3-pass / 1-pass
   int kchunk3 = 1, kchunk1 = 0;
   int group_m = 16;             // GEMM tile rasterization group (tile rows)
+  bool autotune = true;         // TN_AUTOTUNE=0: SIMT steps use the heuristic kernel variant
+  int simt_force = -1;          // TN_SIMT_VARIANT=v: every SIMT step uses variant v (tests)
   bool debug_plan = false;      // TN_DEBUG_PLAN=1: print operand layouts while planning
   // network
   bool loaded = false, pathed = false, planned = false;
@@ -1373,8 +1376,31 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
     for (size_t s = 0; s < c->steps.size(); ++s) {
       StepPlan& sp = c->steps[s];
       if (!sp.tc) {
+        // first execution of an HBM-bound SIMT step: time every kernel variant on the
+        // live operands (the step is idempotent unless it accumulates) and keep the
+        // fastest for the following slices
+        const int nv = tn::einsum_variants(sp.hdesc);
+        if (sp.simt_variant < 0 && c->autotune && c->simt_force < 0 && nv > 1 && !sp.hdesc.acc && sp.tmc > 64e6) {
+          cudaEvent_t ev[2 * 8];
+          for (int v = 0; v < 2 * nv; ++v) TN_CUDA(cudaEventCreate(&ev[v]));
+          for (int v = 0; v < nv; ++v) {
+            TN_CUDA(cudaEventRecord(ev[2 * v], sm));
+            TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, v));
+            TN_CUDA(cudaEventRecord(ev[2 * v + 1], sm));
+          }
+          TN_CUDA(cudaEventSynchronize(ev[2 * nv - 1]));
+          float best = 1e30f;
+          for (int v = 0; v < nv; ++v) {
+            float ms = 0.f;
+            TN_CUDA(cudaEventElapsedTime(&ms, ev[2 * v], ev[2 * v + 1]));
+            if (ms < best) { best = ms; sp.simt_variant = v; }
+          }
+          for (int v = 0; v < 2 * nv; ++v) cudaEventDestroy(ev[v]);
+        }
+        int var = sp.simt_variant < 0 ? 0 : sp.simt_variant;
+        if (c->simt_force >= 0) var = std::min(c->simt_force, nv - 1);
         Timer tm(c, 2, sp.tcc, sp.tmc, (int)s);
-        TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm));
+        TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, var));
       } else {
         const int ps = passes[s];
         const int planes = ps == 3 ? 4 : 2;
@@ -1531,6 +1557,8 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   // 1-pass: whole K in TMEM (promoting every 4 k-blocks costs 10 % and only moves the
   // all-1-pass C4 error from 2.9e-3 to 2.3e-3: fp16 operand rounding dominates there)
   c->kchunk1 = env_int("TN_KCHUNK1", 0);
+  c->autotune = env_int("TN_AUTOTUNE", 1) != 0;
+  c->simt_force = env_int("TN_SIMT_VARIANT", -1);
   c->group_m = env_int("TN_GEMM_GROUP", 8);   // best of {1,8,16,32} on 8192^2 x 16384
   *out = c;
   return TN_OK;

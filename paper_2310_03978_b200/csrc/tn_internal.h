@@ -120,8 +120,10 @@ struct SliceDesc {
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
                         const int64_t* leaf_off, cudaStream_t s);
+// variant: kernel variant of the SIMT mode (0 = heuristic); einsum_variants() = how many
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
-                          const int64_t* leaf_off, cudaStream_t s);
+                          const int64_t* leaf_off, cudaStream_t s, int variant = 0);
+int einsum_variants(const EinsumDesc& host_desc);
 cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
                               cudaStream_t s);
 cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);

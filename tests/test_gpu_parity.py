@@ -130,6 +130,11 @@ ROUTES = {
     "simt_modes": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_DOT_MIN_K": "2",
                    "TN_DOT_MAX_OUT": "16"},
     "simt_wide": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SKINNY_MAX_SMALL": "0"},
+    "simt_variant1": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "1"},
+    "simt_variant2": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "2"},
+    "simt_variant3": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "3"},
+    "simt_wide_variant1": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SKINNY_MAX_SMALL": "0",
+                           "TN_SIMT_VARIANT": "1"},
     "tc": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2"},
     "tc_deep": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "100000", "TN_TC_MIN_K": "2",
                 "TN_TC_DEEP_K": "4"},
