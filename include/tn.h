@@ -142,6 +142,8 @@ typedef struct {
   int64_t device_bytes;      /* device memory held by the plan                           */
   int64_t arena_bytes;       /* liveness-planned intermediate arena                      */
   int64_t scratch_bytes;     /* fp16 operand-plane scratch of the largest tensor-core step */
+  int64_t graph_replays;     /* slices executed by replaying the captured per-slice CUDA
+                                graph (every slice after the first; TN_GRAPHS=0 disables) */
 } tn_info;
 TN_API tn_status tn_get_info(tn_ctx* ctx, tn_info* info);
 

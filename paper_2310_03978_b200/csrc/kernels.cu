@@ -68,6 +68,10 @@ __global__ void slice_select_kernel(const SliceDesc* __restrict__ d) {
   if (threadIdx.x == 0) *d->counter = t0 + 1;
 }
 
+// first slice index of a tn_contract range, passed by value (a pinned-host copy
+// would read the host word at execution time, after later calls overwrote it)
+__global__ void set_counter_kernel(int64_t* counter, int64_t value) { *counter = value; }
+
 // ---------------------------------------------------------------- operand prep
 // Power-of-two exponent s with absmax·2^s in [2^14, 2^15) (inside the fp16 range,
 // PAPER.md L403 "dynamic scaling"); block 0 publishes it for the GEMM epilogue.
@@ -973,6 +977,11 @@ int grid_for(int64_t total, int threads) {
 }
 
 }  // namespace
+
+cudaError_t launch_set_counter(int64_t* counter, int64_t value, cudaStream_t s) {
+  set_counter_kernel<<<1, 1, 0, s>>>(counter, value);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
   slice_select_kernel<<<1, 256, 0, s>>>(d_desc);

@@ -118,6 +118,13 @@ struct tn_ctx {
   int kchunk3 = 1, kchunk1 = 0;
   int group_m = 16;             // GEMM tile rasterization group (tile rows)
   bool autotune = true;         // TN_AUTOTUNE=0: SIMT steps use the heuristic kernel variant
+  // CUDA graph of one slice's launch sequence (TN_GRAPHS=0 disables)
+  bool use_graphs = true, tuned = false;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int g_prec = -1, g_topk = -1;
+  int64_t graph_launches = 0;
+  int64_t g_launch[4] = {0, 0, 0, 0};   // kernel launches per family inside the graph
   int simt_force = -1;          // TN_SIMT_VARIANT=v: every SIMT step uses variant v (tests)
   bool debug_plan = false;      // TN_DEBUG_PLAN=1: print operand layouts while planning
   // network
@@ -162,7 +169,6 @@ struct tn_ctx {
   int* d_scales = nullptr;
   int64_t* d_leaf_off = nullptr;
   int64_t* d_counter = nullptr;
-  int64_t* h_counter = nullptr;
   int32_t* d_out_pos = nullptr;
   tn::SliceDesc* d_slice_desc = nullptr;
   int32_t* d_terms_i = nullptr;
@@ -207,16 +213,18 @@ int64_t index_in(const std::vector<uint64_t>& t, uint64_t v) {
 
 void free_dev(tn_ctx* c) {
   if (c->host_only) { c->planned = false; return; }
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  c->tuned = false;
+  c->g_prec = c->g_topk = -1;
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
                   c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (c->h_counter) cudaFreeHost(c->h_counter);
   c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
   c->d_absmax = nullptr; c->d_scales = nullptr; c->d_leaf_off = nullptr; c->d_counter = nullptr;
   c->d_out_pos = nullptr; c->d_slice_desc = nullptr; c->d_terms_i = nullptr; c->d_terms_s = nullptr;
-  c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr; c->h_counter = nullptr;
+  c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr;
   c->d_partial = nullptr;
   c->d_gt = nullptr;
   c->planned = false;
@@ -988,7 +996,6 @@ tn_status build_plan(tn_ctx* c) {
   if ((st = dev_alloc(c, &c->d_prep, (size_t)std::max(n_prep, 1)))) return st;
   if ((st = dev_alloc(c, &c->d_one, 1))) return st;
   if ((st = dev_alloc(c, &c->d_partial, (size_t)std::max<int64_t>(partial_elems, 2)))) return st;
-  TN_CUDA(cudaMallocHost(&c->h_counter, sizeof(int64_t)));
   if (!tables.empty())
     TN_CUDA(cudaMemcpyAsync(c->d_tables, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice, sm));
   TN_CUDA(cudaMemcpyAsync(c->d_out_pos, c->out_pos.data(), c->out_pos.size() * 4,
@@ -1338,22 +1345,77 @@ struct Timer {
   double flops, bytes;
   int step;
   cudaEvent_t a{}, b{};
-  Timer(tn_ctx* c_, int f, double fl, double by, int st = -1)
-      : c(c_), family(f), flops(fl), bytes(by), step(st) {
+  cudaStream_t sm;
+  Timer(tn_ctx* c_, int f, double fl, double by, int st = -1, cudaStream_t s = nullptr)
+      : c(c_), family(f), flops(fl), bytes(by), step(st), sm(s ? s : c_->stream) {
     c->stats[f].launches++;
     if (c->profiling) {
       cudaEventCreate(&a);
       cudaEventCreate(&b);
-      cudaEventRecord(a, c->stream);
+      cudaEventRecord(a, sm);
     }
   }
   ~Timer() {
     if (c->profiling) {
-      cudaEventRecord(b, c->stream);
+      cudaEventRecord(b, sm);
       c->pending.push_back({a, b, family, flops, bytes, step});
     }
   }
 };
+
+// One slice: slice select (a2) then every path step (a3-a8) on stream `sm`.  The
+// slice index lives in device memory and advances inside slice_select, so the same
+// launch sequence serves every slice (and is what the CUDA graph records).
+tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t sm) {
+  {
+    Timer tm(c, 3, 0, 0, -1, sm);
+    TN_CUDA(tn::launch_slice_select(c->d_slice_desc, sm));
+  }
+  for (size_t s = 0; s < c->steps.size(); ++s) {
+    StepPlan& sp = c->steps[s];
+    if (!sp.tc) {
+      // first execution of an HBM-bound SIMT step: time every kernel variant on the
+      // live operands (the step is idempotent unless it accumulates) and keep the
+      // fastest for the following slices
+      const int nv = tn::einsum_variants(sp.hdesc);
+      if (sp.simt_variant < 0 && c->autotune && c->simt_force < 0 && nv > 1 && !sp.hdesc.acc && sp.tmc > 64e6) {
+        cudaEvent_t ev[2 * 8];
+        for (int v = 0; v < 2 * nv; ++v) TN_CUDA(cudaEventCreate(&ev[v]));
+        for (int v = 0; v < nv; ++v) {
+          TN_CUDA(cudaEventRecord(ev[2 * v], sm));
+          TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, v));
+          TN_CUDA(cudaEventRecord(ev[2 * v + 1], sm));
+        }
+        TN_CUDA(cudaEventSynchronize(ev[2 * nv - 1]));
+        float best = 1e30f;
+        for (int v = 0; v < nv; ++v) {
+          float ms = 0.f;
+          TN_CUDA(cudaEventElapsedTime(&ms, ev[2 * v], ev[2 * v + 1]));
+          if (ms < best) { best = ms; sp.simt_variant = v; }
+        }
+        for (int v = 0; v < 2 * nv; ++v) cudaEventDestroy(ev[v]);
+      }
+      int var = sp.simt_variant < 0 ? 0 : sp.simt_variant;
+      if (c->simt_force >= 0) var = std::min(c->simt_force, nv - 1);
+      Timer tm(c, 2, sp.tcc, sp.tmc, (int)s, sm);
+      TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, var));
+    } else {
+      const int ps = passes[s];
+      const int planes = ps == 3 ? 4 : 2;
+      for (int side = 0; side < 2; ++side) {
+        Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes), (int)s, sm);
+        TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
+                                sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm));
+      }
+      tn::GemmArgs ga = sp.gemm;
+      ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
+      ga.group_m = c->group_m;
+      Timer tm(c, 0, sp.tcc, sp.tmc, (int)s, sm);
+      TN_CUDA(tn::launch_gemm(ga, ps, c->num_sms, sm));
+    }
+  }
+  return TN_OK;
+}
 
 tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int topk) {
   cudaStream_t sm = c->stream;
@@ -1366,56 +1428,42 @@ tn_status run_slices(tn_ctx* c, int64_t t0, int64_t t1, tn_precision prec, int t
                      [&](int a, int b) { return c->steps[a].tcc > c->steps[b].tcc; });
     for (int r = 0; r < (int)tcs.size() && r < topk; ++r) passes[tcs[r]] = 1;
   }
-  *c->h_counter = t0;
-  TN_CUDA(cudaMemcpyAsync(c->d_counter, c->h_counter, sizeof(int64_t), cudaMemcpyHostToDevice, sm));
+  TN_CUDA(tn::launch_set_counter(c->d_counter, t0, sm));
   for (int64_t t = t0; t < t1; ++t) {
-    {
-      Timer tm(c, 3, 0, 0);
-      TN_CUDA(tn::launch_slice_select(c->d_slice_desc, sm));
+    // After the first slice (kernel attributes set, SIMT variants tuned) the per-slice
+    // launch sequence (~500 launches for C4) is recorded once per precision setting
+    // into a CUDA graph on a private capture stream and replayed on the caller's stream.
+    const bool graph = c->use_graphs && c->tuned && !c->profiling;
+    if (!graph) {
+      tn_status st = launch_slice(c, passes, sm);
+      if (st) return st;
+      c->tuned = true;
+      continue;
     }
-    for (size_t s = 0; s < c->steps.size(); ++s) {
-      StepPlan& sp = c->steps[s];
-      if (!sp.tc) {
-        // first execution of an HBM-bound SIMT step: time every kernel variant on the
-        // live operands (the step is idempotent unless it accumulates) and keep the
-        // fastest for the following slices
-        const int nv = tn::einsum_variants(sp.hdesc);
-        if (sp.simt_variant < 0 && c->autotune && c->simt_force < 0 && nv > 1 && !sp.hdesc.acc && sp.tmc > 64e6) {
-          cudaEvent_t ev[2 * 8];
-          for (int v = 0; v < 2 * nv; ++v) TN_CUDA(cudaEventCreate(&ev[v]));
-          for (int v = 0; v < nv; ++v) {
-            TN_CUDA(cudaEventRecord(ev[2 * v], sm));
-            TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, v));
-            TN_CUDA(cudaEventRecord(ev[2 * v + 1], sm));
-          }
-          TN_CUDA(cudaEventSynchronize(ev[2 * nv - 1]));
-          float best = 1e30f;
-          for (int v = 0; v < nv; ++v) {
-            float ms = 0.f;
-            TN_CUDA(cudaEventElapsedTime(&ms, ev[2 * v], ev[2 * v + 1]));
-            if (ms < best) { best = ms; sp.simt_variant = v; }
-          }
-          for (int v = 0; v < 2 * nv; ++v) cudaEventDestroy(ev[v]);
-        }
-        int var = sp.simt_variant < 0 ? 0 : sp.simt_variant;
-        if (c->simt_force >= 0) var = std::min(c->simt_force, nv - 1);
-        Timer tm(c, 2, sp.tcc, sp.tmc, (int)s);
-        TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, var));
-      } else {
-        const int ps = passes[s];
-        const int planes = ps == 3 ? 4 : 2;
-        for (int side = 0; side < 2; ++side) {
-          Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes), (int)s);
-          TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
-                                  sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm));
-        }
-        tn::GemmArgs ga = sp.gemm;
-        ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
-        ga.group_m = c->group_m;
-        Timer tm(c, 0, sp.tcc, sp.tmc, (int)s);
-        TN_CUDA(tn::launch_gemm(ga, ps, c->num_sms, sm));
+    if (!c->gexec || c->g_prec != (int)prec || c->g_topk != topk) {
+      if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+      if (!c->cap_stream) TN_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+      int64_t before[4];
+      for (int f = 0; f < 4; ++f) before[f] = c->stats[f].launches;
+      TN_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+      tn_status st = launch_slice(c, passes, c->cap_stream);
+      for (int f = 0; f < 4; ++f) {   // a capture is not an execution: count launches per replay
+        c->g_launch[f] = c->stats[f].launches - before[f];
+        c->stats[f].launches = before[f];
       }
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+      if (st) { if (g) cudaGraphDestroy(g); return st; }
+      if (e != cudaSuccess) return fail(TN_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return fail(TN_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+      c->g_prec = (int)prec;
+      c->g_topk = topk;
     }
+    TN_CUDA(cudaGraphLaunch(c->gexec, sm));
+    c->graph_launches++;
+    for (int f = 0; f < 4; ++f) c->stats[f].launches += c->g_launch[f];
   }
   return TN_OK;
 }
@@ -1558,6 +1606,7 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   // all-1-pass C4 error from 2.9e-3 to 2.3e-3: fp16 operand rounding dominates there)
   c->kchunk1 = env_int("TN_KCHUNK1", 0);
   c->autotune = env_int("TN_AUTOTUNE", 1) != 0;
+  c->use_graphs = env_int("TN_GRAPHS", 1) != 0;
   c->simt_force = env_int("TN_SIMT_VARIANT", -1);
   c->group_m = env_int("TN_GEMM_GROUP", 8);   // best of {1,8,16,32} on 8192^2 x 16384
   *out = c;
@@ -1571,6 +1620,7 @@ void tn_destroy(tn_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   free_dev(c);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->d_leaf) cudaFree(c->d_leaf);
   if (c->h_leaf_pinned) cudaFreeHost(c->h_leaf_pinned);
   delete c;
@@ -1770,6 +1820,7 @@ tn_status tn_get_info(tn_ctx* c, tn_info* info) {
   info->device_bytes = c->device_bytes;
   info->arena_bytes = c->arena_elems * (int64_t)sizeof(float2);
   info->scratch_bytes = c->scratch_bytes;
+  info->graph_replays = c->graph_launches;
   return TN_OK;
 }
 

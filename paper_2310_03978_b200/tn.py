@@ -42,7 +42,8 @@ class Info(C.Structure):
                 ("n_tc_steps", C.c_int32), ("flops_per_slice", C.c_double),
                 ("tc_flops_per_slice", C.c_double), ("bytes_per_slice", C.c_double),
                 ("peak_elements", C.c_double), ("device_bytes", C.c_int64),
-                ("arena_bytes", C.c_int64), ("scratch_bytes", C.c_int64)]
+                ("arena_bytes", C.c_int64), ("scratch_bytes", C.c_int64),
+                ("graph_replays", C.c_int64)]
 
 
 class KernelStats(C.Structure):

@@ -207,6 +207,34 @@ def test_per_slice_parity_and_accumulation(ctx, force_tc):
     c.close()
 
 
+@pytest.mark.parametrize("route", ["default", "tc"])
+def test_cuda_graph_replay_matches_direct_launches(ctx, route, monkeypatch):
+    """Slices after the first replay a captured CUDA graph of the per-slice launch
+    sequence; the result must equal direct launches (TN_GRAPHS=0) and the oracle."""
+    for k, v in ROUTES[route].items():
+        monkeypatch.setenv(k, v)
+    w = configs.small(grid=(3, 4), cycles=8, mode="sparse", n_samples=64, n_slices=8, seed=5)
+    ref = oracle.contract(w.net, w.path, w.sliced, w.samples)
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(w.net, w.samples, w.path, w.sliced)
+    for t in range(c.n_slices):            # one slice per call, as bench.py does
+        c.contract(t, t + 1)
+    got = c.sum_slices_host()
+    replays = c.info()["graph_replays"]
+    c.contract(0, 3, precision="mixed")    # a second precision setting captures its own graph
+    c.close()
+    assert replays >= 6, replays
+    monkeypatch.setenv("TN_GRAPHS", "0")
+    d = Contraction(device=0, stream=torch.cuda.current_stream())
+    d.setup(w.net, w.samples, w.path, w.sliced)
+    d.contract(0, d.n_slices)
+    direct = d.sum_slices_host()
+    assert d.info()["graph_replays"] == 0
+    d.close()
+    assert rel_l2(got, direct) <= 1e-12
+    assert rel_l2(got, ref) <= EXT_TOL
+
+
 def test_c1_vs_statevector(ctx):
     for mode in ["single", "full"]:
         w = configs.c1(mode)
