@@ -63,6 +63,10 @@ struct Cfg {
       STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BN * 8 /*column offsets*/;
   static constexpr int TILE_M = PAIR ? 2 * BM : BM;
 };
+// per-warp staging tile for plane outputs whose unit-stride dim is a row dim
+// (8 epilogue warps only: 16 would exceed the 227 KB shared-memory limit)
+template <int EW>
+constexpr int stage_bytes() { return EW == 8 ? EW * 32 * 9 * 8 : 0; }
 
 // instruction descriptor, kind::f16: D=f32 (bits 4-5 = 1), A=B=f16, K-major,
 // N>>3 at bits 17-22, M>>4 at bits 24-28; bit 13 = negate A.
@@ -240,6 +244,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
   // general output map: per-tile column offsets, double-buffered by tile parity
   int64_t* noff_tab = reinterpret_cast<int64_t*>(smem + STAGES * C::STAGE_BYTES + 256);
+  float2* stage_buf = reinterpret_cast<float2*>(noff_tab + 2 * BN);   // [warp][32][9]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -427,6 +432,16 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
     const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const float scale = ldexpf(1.0f, -(*args.scaleA + *args.scaleB));
+    // fused plane output: consumer exponent sC = max(bound, delayed scaling); the planes
+    // hold x * 2^sC = acc * 2^(sC - sA - sB)
+    int plane_sc = 0;
+    if (args.out_planes) {
+      const int sab = *args.scaleA + *args.scaleB;
+      plane_sc = max(sab + args.plane_exp, *args.plane_pexp);
+      if (blockIdx.x == 0 && threadIdx.x == 64) *args.plane_scale_out = plane_sc;
+      plane_sc -= sab;
+    }
+    bool plane_ovf = false;
     float amax = 0.f;
     int cb = 0;
     uint32_t cphase = 0;
@@ -482,6 +497,86 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
           tab[et] = off;
         }
         asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
+        if (args.out_planes) {
+          // ---- fused consumer prep: 8 destination-contiguous columns -> one 16-B vector
+          // per fp16 plane (RN hi, RN lo = rn(x - hi), Eq. 8), scaled by 2^plane_exp
+          if (n0 < args.N && (m < args.M || (EW == 8 && args.planes_rows))) {
+            // rows mode: M is a multiple of 8 row groups, so a group is all-valid or all-padding
+            int64_t t = m < args.M ? m : 0, moff = 0;
+            for (int q = args.n_po - 1; q >= 0; --q) {
+              const int sh = args.po_sh[q];
+              moff += (t & ((int64_t(1) << sh) - 1)) * args.po_str[q];
+              t >>= sh;
+            }
+            const int64_t rb = m < args.M ? (int64_t)j * args.M * (int64_t)args.N + moff : -1;
+            const int64_t* tc = tab + half * WC;
+            __half* P = reinterpret_cast<__half*>(args.C);
+            const int64_t pe = args.plane_elems;
+            const float ps = ldexpf(1.0f, plane_sc);
+            if (EW == 8 && args.planes_rows) {
+              // unit-stride plane dim = the 8 lowest row bits: stage 8 columns of the
+              // warp's 32 rows in smem, then lane (group g, column c) writes rows
+              // 8g..8g+7 of column c as one 16-B vector per plane
+              float2* buf = stage_buf + (warp - 2) * 32 * 9;
+              const int g = lane >> 3, cc = lane & 7;
+              const int64_t gb = __shfl_sync(0xffffffffu, rb, 8 * g);
+#pragma unroll
+              for (int i = 0; i < WC; i += 8) {
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                  buf[lane * 9 + jj] = make_float2(sr[i + jj] * ps, si[i + jj] * ps);
+                  if (rb >= 0 && n0 + i + jj < args.N)
+                    amax = fmaxf(amax, fmaxf(fabsf(sr[i + jj]), fabsf(si[i + jj])));
+                }
+                __syncwarp();
+                __align__(16) __half hr[8], hi[8], lr[8], li[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                  const float2 x = buf[(8 * g + jj) * 9 + cc];
+                  hr[jj] = __float2half_rn(x.x);
+                  hi[jj] = __float2half_rn(x.y);
+                  plane_ovf |= fmaxf(fabsf(x.x), fabsf(x.y)) >= 65504.f;
+                  lr[jj] = __float2half_rn(x.x - __half2float(hr[jj]));
+                  li[jj] = __float2half_rn(x.y - __half2float(hi[jj]));
+                }
+                __syncwarp();
+                if (gb >= 0 && n0 + i + cc < args.N) {
+                  const int64_t a0 = gb + tc[i + cc];
+                  *reinterpret_cast<uint4*>(P + a0) = *reinterpret_cast<const uint4*>(hr);
+                  *reinterpret_cast<uint4*>(P + pe + a0) = *reinterpret_cast<const uint4*>(hi);
+                  if (args.out_nplanes == 4) {
+                    *reinterpret_cast<uint4*>(P + 2 * pe + a0) = *reinterpret_cast<const uint4*>(lr);
+                    *reinterpret_cast<uint4*>(P + 3 * pe + a0) = *reinterpret_cast<const uint4*>(li);
+                  }
+                }
+              }
+              continue;
+            }
+#pragma unroll
+            for (int i = 0; i < WC; i += 8) {
+              if (n0 + i >= args.N) continue;
+              const int64_t a0 = rb + tc[i];
+              __align__(16) __half hr[8], hi[8], lr[8], li[8];
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const float xr = sr[i + jj] * ps, xi = si[i + jj] * ps;
+                amax = fmaxf(amax, fmaxf(fabsf(sr[i + jj]), fabsf(si[i + jj])));
+                plane_ovf |= fmaxf(fabsf(xr), fabsf(xi)) >= 65504.f;
+                hr[jj] = __float2half_rn(xr);
+                hi[jj] = __float2half_rn(xi);
+                lr[jj] = __float2half_rn(xr - __half2float(hr[jj]));
+                li[jj] = __float2half_rn(xi - __half2float(hi[jj]));
+              }
+              *reinterpret_cast<uint4*>(P + a0) = *reinterpret_cast<const uint4*>(hr);
+              *reinterpret_cast<uint4*>(P + pe + a0) = *reinterpret_cast<const uint4*>(hi);
+              if (args.out_nplanes == 4) {
+                *reinterpret_cast<uint4*>(P + 2 * pe + a0) = *reinterpret_cast<const uint4*>(lr);
+                *reinterpret_cast<uint4*>(P + 3 * pe + a0) = *reinterpret_cast<const uint4*>(li);
+              }
+            }
+          }
+          continue;
+        }
         if (m < args.M && n0 < args.N) {
           int64_t t = m, moff = 0;
           for (int q = args.n_po - 1; q >= 0; --q) {
@@ -551,6 +646,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
         }
       }
     }
+    if (args.out_planes) {
+      amax *= scale;       // raw accumulator maxima -> true values (absmax_out below)
+      if (__any_sync(0xffffffffu, plane_ovf) && lane == 0) atomicOr(args.overflow, 1);
+    }
     if (args.absmax_out) {
       for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
       if (lane == 0 && amax > 0.f) atomicMax(args.absmax_out, __float_as_uint(amax));
@@ -572,7 +671,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
 template <int PASSES, int EW, bool PAIR>
 cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
   static bool attr_set = false;
-  const int smem = Cfg<PASSES, PAIR>::SMEM_BYTES;
+  const int smem = Cfg<PASSES, PAIR>::SMEM_BYTES + stage_bytes<EW>();
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES, EW, PAIR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -607,7 +706,9 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
   }
 }
 
-int epi_warps() {   // TN_GEMM_EPI = 8 | 16 epilogue warps
+}  // namespace
+
+int gemm_epi_warps() {   // TN_GEMM_EPI = 8 | 16 epilogue warps (single-CTA kernel; pairs use 8)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TN_GEMM_EPI");
@@ -615,6 +716,8 @@ int epi_warps() {   // TN_GEMM_EPI = 8 | 16 epilogue warps
   }
   return v;
 }
+
+namespace {
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -649,7 +752,7 @@ bool gemm_pair_ok(const GemmArgs& a, int min_m) {
 cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s) {
   if (a.use_pair)
     return passes == 3 ? launch_impl<3, 8, true>(a, num_sms, s) : launch_impl<1, 8, true>(a, num_sms, s);
-  if (epi_warps() == 16)
+  if (gemm_epi_warps() == 16)
     return passes == 3 ? launch_impl<3, 16, false>(a, num_sms, s) : launch_impl<1, 16, false>(a, num_sms, s);
   return passes == 3 ? launch_impl<3, 8, false>(a, num_sms, s) : launch_impl<1, 8, false>(a, num_sms, s);
 }

@@ -63,7 +63,14 @@ __global__ void slice_select_kernel(const SliceDesc* __restrict__ d) {
       if (d->term_leaf[q] == l) off += digit[d->term_p[q]] * d->term_stride[q];
     d->leaf_off[l] = off;
   }
-  for (int a = threadIdx.x; a < d->absmax_count; a += blockDim.x) d->absmax[d->absmax_first + a] = 0u;
+  for (int a = threadIdx.x; a < d->absmax_count; a += blockDim.x) {
+    const unsigned h = max(d->hist[a], d->absmax[d->absmax_first + a]);   // finished slice
+    d->hist[a] = h;
+    int e = 0;
+    if (h) frexpf(__uint_as_float(h), &e);
+    d->pexp[a] = h ? 11 - e : -100000;
+    d->absmax[d->absmax_first + a] = 0u;
+  }
   __syncthreads();
   if (threadIdx.x == 0) *d->counter = t0 + 1;
 }

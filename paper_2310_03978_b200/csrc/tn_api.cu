@@ -7,6 +7,7 @@
 #include "tn.h"
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -93,6 +94,12 @@ struct StepPlan {
   bool out_gen = false;
   std::vector<VDim> po, qo;
   int simt_variant = -1;        // SIMT kernel variant chosen by the first-slice autotuner
+  // fused operand prep: side s of this tensor-core step
+  // reads fp16 planes its producer's epilogue wrote (no prep launch); planes_consumer =
+  // the step whose planes this step's epilogue writes (-1: writes complex64)
+  bool skip_prep[2] = {false, false};
+  int planes_consumer = -1;
+  tn::GemmArgs gemm_plain;      // the step's GEMM without fusion (first, absmax-seeding slice)
 };
 
 struct KStats {
@@ -177,6 +184,9 @@ struct tn_ctx {
   tn::PrepDesc* d_prep = nullptr;
   float2* d_one = nullptr;
   double* d_partial = nullptr;     // split-K dot partial sums
+  unsigned* d_hist = nullptr;      // delayed scaling: running output absmax per step
+  int* d_pexp = nullptr;           // delayed scaling: exponent per step (slice_select)
+  int* d_flag = nullptr;           // fused plane overflow flag
   int64_t* d_gt = nullptr;         // general-transposer tile tables
   int64_t device_bytes = 0;
   // profiling
@@ -218,7 +228,8 @@ void free_dev(tn_ctx* c) {
   c->g_prec = c->g_topk = -1;
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
-                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt};
+                  c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt,
+                  c->d_hist, c->d_pexp, c->d_flag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
@@ -227,6 +238,7 @@ void free_dev(tn_ctx* c) {
   c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr;
   c->d_partial = nullptr;
   c->d_gt = nullptr;
+  c->d_hist = nullptr; c->d_pexp = nullptr; c->d_flag = nullptr;
   c->planned = false;
 }
 
@@ -598,6 +610,8 @@ tn_status build_plan(tn_ctx* c) {
   const int group_min_use = env_int("TN_GROUP_MIN_USE", 8);   // route when useful >= 1/this
   const int pair_min_m = tn::gemm_pair_min_m();            // CTA-pair GEMM for M >= this
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
+  const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
+                                                           // (2: column-contiguous case only)
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
 
@@ -630,6 +644,11 @@ tn_status build_plan(tn_ctx* c) {
   // Producers place those bonds last (sorted), so the consumer's operand prep
   // reads long contiguous runs.
   std::vector<std::unordered_set<int64_t>> consumer_k(n_steps);
+  std::vector<int> consumer_step(n_steps, -1);
+  // K order of a step's operands (outer -> inner labels), chosen by the tensor-core
+  // producer of one operand so that its epilogue can write the operand's fp16 planes
+  // in 16-B vectors; default: sorted by label
+  std::vector<std::vector<int64_t>> korder(n_steps);
   {
     std::vector<std::unordered_set<int64_t>> lab(n_leaves);
     std::vector<int> producer(n_leaves, -1);
@@ -640,8 +659,8 @@ tn_status build_plan(tn_ctx* c) {
       const int i = c->path[s].first, j = c->path[s].second;
       std::unordered_set<int64_t> shared;
       for (int64_t x : lab[i]) if (lab[j].count(x)) shared.insert(x);
-      if (producer[i] >= 0) consumer_k[producer[i]] = shared;
-      if (producer[j] >= 0) consumer_k[producer[j]] = shared;
+      if (producer[i] >= 0) { consumer_k[producer[i]] = shared; consumer_step[producer[i]] = s; }
+      if (producer[j] >= 0) { consumer_k[producer[j]] = shared; consumer_step[producer[j]] = s; }
       std::unordered_set<int64_t> out;
       for (int64_t x : lab[i]) if (!shared.count(x)) out.insert(x);
       for (int64_t x : lab[j]) if (!shared.count(x)) out.insert(x);
@@ -873,10 +892,33 @@ tn_status build_plan(tn_ctx* c) {
       for (auto& d : P) gen = gen && p2(d.ext);
       for (auto& d : Q) gen = gen && p2(d.ext);
       if (gen) {
-        std::vector<VDim> con;
-        for (auto& d : P) (kc.count(d.label) ? con : od).push_back({d.label, d.ext, 0});
-        for (auto& d : Q) (kc.count(d.label) ? con : od).push_back({d.label, d.ext, 0});
-        std::sort(con.begin(), con.end(), [](const VDim& a, const VDim& b) { return a.label < b.label; });
+        std::vector<VDim> con, conp, conq;
+        for (auto& d : P) (kc.count(d.label) ? conp : od).push_back({d.label, d.ext, 0});
+        for (auto& d : Q) (kc.count(d.label) ? conq : od).push_back({d.label, d.ext, 0});
+        auto by_label = [](const VDim& a, const VDim& b) { return a.label < b.label; };
+        std::sort(conp.begin(), conp.end(), by_label);
+        std::sort(conq.begin(), conq.end(), by_label);
+        // innermost: the consumer-contracted bonds of one side (>= 8 elements if possible:
+        // 16-B plane vectors along columns (Q) or rows (P) of this GEMM's tile)
+        int64_t ep = 1, eq = 1;
+        for (auto& d : conp) ep *= d.ext;
+        for (auto& d : conq) eq *= d.ext;
+        const bool q_inner = eq >= 8 || ep < 8;
+        for (auto& d : (q_inner ? conp : conq)) con.push_back(d);
+        for (auto& d : (q_inner ? conq : conp)) con.push_back(d);
+        if (consumer_step[s] >= 0) {
+          std::vector<int64_t>& ko = korder[consumer_step[s]];
+          if (ko.empty()) {            // the consumer's first tensor-core producer decides
+            for (auto& d : con) ko.push_back(d.label);
+          } else {                     // the other operand follows it (same K order)
+            auto rank = [&](int64_t l) {
+              for (size_t q = 0; q < ko.size(); ++q) if (ko[q] == l) return (int64_t)q;
+              return (int64_t)ko.size();
+            };
+            std::stable_sort(con.begin(), con.end(),
+                             [&](const VDim& x, const VDim& y) { return rank(x.label) < rank(y.label); });
+          }
+        }
         od.insert(od.end(), con.begin(), con.end());
         std::vector<VDim> tmp = od;
         contiguous_strides(tmp);
@@ -996,6 +1038,11 @@ tn_status build_plan(tn_ctx* c) {
   if ((st = dev_alloc(c, &c->d_prep, (size_t)std::max(n_prep, 1)))) return st;
   if ((st = dev_alloc(c, &c->d_one, 1))) return st;
   if ((st = dev_alloc(c, &c->d_partial, (size_t)std::max<int64_t>(partial_elems, 2)))) return st;
+  if ((st = dev_alloc(c, &c->d_hist, (size_t)n_steps))) return st;
+  if ((st = dev_alloc(c, &c->d_pexp, (size_t)n_steps))) return st;
+  if ((st = dev_alloc(c, &c->d_flag, 1))) return st;
+  TN_CUDA(cudaMemsetAsync(c->d_hist, 0, n_steps * sizeof(unsigned), sm));
+  TN_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), sm));
   if (!tables.empty())
     TN_CUDA(cudaMemcpyAsync(c->d_tables, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice, sm));
   TN_CUDA(cudaMemcpyAsync(c->d_out_pos, c->out_pos.data(), c->out_pos.size() * 4,
@@ -1031,6 +1078,8 @@ tn_status build_plan(tn_ctx* c) {
     sd.absmax = c->d_absmax;
     sd.absmax_first = n_leaves;
     sd.absmax_count = n_steps;
+    sd.hist = c->d_hist;
+    sd.pexp = c->d_pexp;
     TN_CUDA(cudaMemcpyAsync(c->d_slice_desc, &sd, sizeof(sd), cudaMemcpyHostToDevice, sm));
   }
   }  // !host_only
@@ -1053,9 +1102,17 @@ tn_status build_plan(tn_ctx* c) {
     live[t] = v;
   }
   char errbuf[256];
+  std::unordered_map<int, int> producer_of;     // live tensor id -> producing step
+  std::vector<std::array<int, 2>> side_producer(n_steps, {-1, -1});   // per TC side
   for (int s = 0; s < n_steps; ++s) {
     StepPlan& sp = c->steps[s];
     View A = live[sp.i], B = live[sp.j];
+    if (sp.tc)
+      for (int side = 0; side < 2; ++side) {
+        const int id = ((side == 0) != sp.swap) ? sp.i : sp.j;
+        auto it = producer_of.find(id);
+        side_producer[s][side] = it == producer_of.end() ? -1 : it->second;
+      }
     std::unordered_set<int64_t> lb;
     for (auto& d : B.dims) if (d.label != GROUP) lb.insert(d.label);
     std::vector<VDim> FA, FB;
@@ -1063,8 +1120,8 @@ tn_status build_plan(tn_ctx* c) {
     std::unordered_set<int64_t> kset;
     VDim gA{GROUP, 1, 0}, gB{GROUP, 1, 0};
     {
-      // canonical K order: sorted by label (tensor-core producers write their
-      // consumer's contracted bonds innermost in this order)
+      // canonical K order: the order a tensor-core producer wrote the contracted bonds
+      // in (korder), else sorted by label
       std::vector<std::pair<int64_t, KDim>> kl;
       for (auto& d : A.dims)
         if (d.label != GROUP && lb.count(d.label)) {
@@ -1073,10 +1130,18 @@ tn_status build_plan(tn_ctx* c) {
           for (auto& e : B.dims) if (e.label == d.label) sb = e.stride;
           kl.push_back({d.label, {d.ext, d.stride, sb}});
         }
-      std::sort(kl.begin(), kl.end(),
-                [](const std::pair<int64_t, KDim>& a, const std::pair<int64_t, KDim>& b) {
-                  return a.first < b.first;
-                });
+      {
+        const std::vector<int64_t>& ko = korder[s];
+        auto rank = [&](int64_t l) {
+          for (size_t q = 0; q < ko.size(); ++q) if (ko[q] == l) return (int64_t)q;
+          return (int64_t)ko.size();
+        };
+        std::sort(kl.begin(), kl.end(),
+                  [&](const std::pair<int64_t, KDim>& a, const std::pair<int64_t, KDim>& b) {
+                    const int64_t ra = rank(a.first), rb = rank(b.first);
+                    return ra != rb ? ra < rb : a.first < b.first;
+                  });
+      }
       for (auto& x : kl) K.push_back(x.second);
     }
     for (auto& d : A.dims) {
@@ -1315,7 +1380,120 @@ tn_status build_plan(tn_ctx* c) {
     }
     live.erase(sp.j);
     live[sp.i] = sp.out;
+    producer_of.erase(sp.j);
+    producer_of[sp.i] = s;
   }
+  // ---- fused plane output (a3 + a6 folded into the producer's GEMM epilogue): a
+  // tensor-core step whose output is a tensor-core operand writes that operand's fp16
+  // planes in the consumer's [G][R][Kpad] layout straight into its arena slot (same
+  // 8 bytes per element as complex64), and the consumer skips that side's prep.
+  for (auto& st_ : c->steps) st_.gemm_plain = st_.gemm;
+  if (fuse_planes)
+    for (int s = 0; s < n_steps; ++s) {
+      StepPlan& cs = c->steps[s];
+      if (!cs.tc || cs.grouped) continue;
+      for (int side = 0; side < 2; ++side) {
+        const int ps = side_producer[s][side];
+        if (ps < 0) continue;
+        StepPlan& pp = c->steps[ps];
+        if (!pp.tc || pp.grouped || pp.final_step || pp.planes_consumer >= 0) continue;
+        if (c->debug_plan) fprintf(stderr, "[tn] fuse candidate %d->%d side %d\n", ps, s, side);
+        const tn::PrepDesc& pd = pds[cs.prep_idx + side];
+        const int64_t Kp = cs.Kpad;
+        auto skip = [&](const char* why) {
+          if (c->debug_plan) fprintf(stderr, "[tn] fuse %d->%d side %d: no (%s)\n", ps, s, side, why);
+        };
+        if (Kp != cs.k || Kp % 8 != 0) { skip("K"); continue; }
+        if (pd.G * pd.R * Kp != pp.out_elems) { skip("size"); continue; }
+        if (pd.G > 1 && pd.g_stride != pd.R * Kp) { skip("group"); continue; }
+        // source (producer complex64 offset) bit weight -> consumer plane-element weight
+        std::unordered_map<int64_t, int64_t> wmap;
+        bool ok = true;
+        auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+        int64_t inner = 1;
+        for (int d = pd.nk - 1; d >= 0 && ok; --d) {
+          ok = p2(pd.k_ext[d]) && p2(pd.k_s[d]);
+          for (int64_t e = 1; ok && e < pd.k_ext[d]; e <<= 1) ok = wmap.emplace(pd.k_s[d] * e, inner * e).second;
+          inner *= pd.k_ext[d];
+        }
+        inner = Kp;
+        for (int d = pd.nr - 1; d >= 0 && ok; --d) {
+          ok = p2(pd.r_ext[d]) && p2(pd.r_s[d]);
+          for (int64_t e = 1; ok && e < pd.r_ext[d]; e <<= 1) ok = wmap.emplace(pd.r_s[d] * e, inner * e).second;
+          inner *= pd.r_ext[d];
+        }
+        if (!ok) { skip("prep dims"); continue; }
+        // the producer's row / column digit maps (outer -> inner), one bit per entry,
+        // re-expressed in plane units, then re-coalesced
+        auto side_dims = [&](bool rows, std::vector<std::pair<int, int64_t>>& out) {
+          const tn::GemmArgs& g = pp.gemm;
+          std::vector<VDim> dims;
+          if (pp.out_gen) {
+            const int n = rows ? g.n_po : g.n_qo;
+            for (int q = 0; q < n; ++q)
+              dims.push_back({0, int64_t(1) << (rows ? g.po_sh[q] : g.qo_sh[q]), rows ? g.po_str[q] : g.qo_str[q]});
+          } else {   // plain [J][M][N]
+            if (rows) dims.push_back({0, (int64_t)g.M, (int64_t)g.N});
+            else dims.push_back({0, (int64_t)g.N, 1});
+          }
+          std::vector<int64_t> bits;   // plane weight per digit bit, inner -> outer
+          for (int q = (int)dims.size() - 1; q >= 0; --q) {
+            if (!p2(dims[q].ext)) return false;
+            for (int64_t e = 1; e < dims[q].ext; e <<= 1) {
+              auto it = wmap.find(dims[q].stride * e);
+              if (it == wmap.end()) return false;
+              bits.push_back(it->second);
+            }
+          }
+          out.clear();                 // coalesce inner -> outer, emit outer -> inner
+          for (int64_t w : bits) {
+            if (!out.empty() && (out.back().second << out.back().first) == w) out.back().first++;
+            else out.push_back({1, w});
+          }
+          std::reverse(out.begin(), out.end());
+          return (int)out.size() <= 16;
+        };
+        std::vector<std::pair<int, int64_t>> po, qo;
+        if (!side_dims(true, po) || !side_dims(false, qo)) { skip("producer dims"); continue; }
+        // 16-B plane vectors: the 8 lowest column indices must be plane-contiguous
+        const bool cols = !qo.empty() && qo.back().second == 1 && qo.back().first >= 3;
+        const bool rows = fuse_planes != 2 && !po.empty() && po.back().second == 1 && po.back().first >= 3 &&
+                          pp.gemm.M % 8 == 0 && (pp.gemm.use_pair || tn::gemm_epi_warps() == 8);
+        if (pp.gemm.N % 8 != 0 || (!cols && !rows)) {
+          skip("no plane-contiguous run of 8 rows or columns");
+          continue;
+        }
+        tn::GemmArgs& g = pp.gemm;
+        g.planes_rows = cols ? 0 : 1;
+        if (c->debug_plan)
+          fprintf(stderr, "[tn] fuse %d->%d side %d: yes (%s, producer K=%lld)\n", ps, s, side, cols ? "cols" : "rows",
+                  (long long)pp.k);
+        g.out_gen = 1;
+        g.out_planes = 1;
+        g.n_po = (int)po.size();
+        g.n_qo = (int)qo.size();
+        for (int q = 0; q < g.n_po; ++q) { g.po_sh[q] = (uint8_t)po[q].first; g.po_str[q] = po[q].second; }
+        for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)qo[q].first; g.qo_str[q] = qo[q].second; }
+        int lk = 0;
+        while ((int64_t(1) << lk) < pp.k) ++lk;
+        g.plane_exp = -16 - lk;
+        g.plane_elems = pp.out_elems;
+        g.plane_scale_out = c->d_scales + 2 * s + side;
+        g.plane_pexp = c->d_pexp + ps;
+        g.overflow = c->d_flag;
+        pp.out_gen = true;
+        pp.planes_consumer = s;
+        cs.skip_prep[side] = true;
+        if (!c->host_only) {
+          const __half* base = reinterpret_cast<const __half*>(c->d_arena + pp.out_off);
+          CUtensorMap* map = side == 0 ? &cs.gemm.mapA : &cs.gemm.mapB;
+          if (!tn::encode_plane_map(map, base, Kp, cs.R[side], cs.G[side], 4, 128, errbuf, sizeof(errbuf)) ||
+              (side == 1 && !tn::encode_plane_map(&cs.gemm.mapB2, base, Kp, cs.R[side], cs.G[side], 4, 64,
+                                                  errbuf, sizeof(errbuf))))
+            return fail(TN_ERR_INTERNAL, errbuf);
+        }
+      }
+    }
   if (c->host_only) {
     c->planned = true;
     return TN_OK;
@@ -1402,14 +1580,18 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
     } else {
       const int ps = passes[s];
       const int planes = ps == 3 ? 4 : 2;
+      // the first slice runs unfused: it seeds the delayed-scaling absmax history
+      const bool fused = c->tuned;
       for (int side = 0; side < 2; ++side) {
+        if (fused && sp.skip_prep[side]) continue;   // planes written by the producer's epilogue
         Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes), (int)s, sm);
         TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
                                 sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm));
       }
-      tn::GemmArgs ga = sp.gemm;
+      tn::GemmArgs ga = fused ? sp.gemm : sp.gemm_plain;
       ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
       ga.group_m = c->group_m;
+      if (fused && sp.planes_consumer >= 0) ga.out_nplanes = passes[sp.planes_consumer] == 3 ? 4 : 2;
       Timer tm(c, 0, sp.tcc, sp.tmc, (int)s, sm);
       TN_CUDA(tn::launch_gemm(ga, ps, c->num_sms, sm));
     }
@@ -1779,12 +1961,26 @@ tn_status tn_reset_accumulator(tn_ctx* c) {
   tn_status st = check_planned(c);
   if (st) return st;
   TN_CUDA(cudaMemsetAsync(c->d_acc, 0, c->acc_elems * sizeof(double2), c->stream));
+  TN_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  return TN_OK;
+}
+
+// A fused producer whose delayed-scaling margin (32x over the largest absmax of the
+// slices before) was exceeded wrote saturated fp16 planes: fail loudly, never return
+// such a sum (rerun with TN_FUSE_PLANES=0).
+tn_status check_plane_overflow(tn_ctx* c) {
+  int flag = 0;
+  TN_CUDA(cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  TN_CUDA(cudaStreamSynchronize(c->stream));
+  if (flag) return fail(TN_ERR_DATA, "fp16 plane overflow in a fused producer epilogue (delayed-scaling "
+                                     "margin exceeded); rerun with TN_FUSE_PLANES=0");
   return TN_OK;
 }
 
 tn_status tn_sum_slices(tn_ctx* c, double* out, int64_t n_out) {
   tn_status st = check_planned(c);
   if (st) return st;
+  if ((st = check_plane_overflow(c))) return st;
   if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
   if (!out) return fail(TN_ERR_USAGE, "out is NULL");
   TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, reinterpret_cast<double2*>(out), n_out, c->stream));
@@ -1794,6 +1990,7 @@ tn_status tn_sum_slices(tn_ctx* c, double* out, int64_t n_out) {
 tn_status tn_sum_slices_host(tn_ctx* c, double* out_host, int64_t n_out) {
   tn_status st = check_planned(c);
   if (st) return st;
+  if ((st = check_plane_overflow(c))) return st;
   if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
   double2* tmp = nullptr;
   TN_CUDA(cudaMallocAsync(&tmp, n_out * sizeof(double2), c->stream));
@@ -1837,11 +2034,12 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
              sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false",
-             sp.tc ? sp.r_fast[0] : -1, sp.tc ? sp.r_fast[1] : -1);
+             sp.tc ? (sp.skip_prep[0] ? -1 : sp.r_fast[0]) : -1,
+             sp.tc ? (sp.skip_prep[1] ? -1 : sp.r_fast[1]) : -1, sp.planes_consumer >= 0 ? "true" : "false");
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";

@@ -102,6 +102,19 @@ struct GemmArgs {
   int32_t out_gen, n_po, n_qo, pad_o;
   uint8_t po_sh[16], qo_sh[16];
   int64_t po_str[16], qo_str[16];
+  // fused consumer prep (a3 + a6 in this epilogue): the output is written directly as the
+  // consumer's K-contiguous fp16 planes (po/qo strides are plane-element strides; C is
+  // the plane base, plane p at C + p*plane_elems halves).  Values are acc * 2^plane_exp
+  // with plane_exp = -16 - ceil(log2 K): |acc| <= K 2^31 for operands scaled below 2^15,
+  // so the planes stay below 2^15 without waiting for the output's absmax; the consumer's
+  // exponent sA + sB + plane_exp goes to *plane_scale_out.
+  int32_t out_planes, out_nplanes, plane_exp;
+  int32_t planes_rows;            // 1: the unit-stride plane dim is the 8 lowest row bits
+                                  // (staged through smem); 0: the 8 lowest column bits
+  int64_t plane_elems;
+  int* plane_scale_out;
+  const int* plane_pexp;          // delayed-scaling exponent (SliceDesc.pexp[step])
+  int* overflow;                  // set when a plane value reaches the fp16 range limit
 };
 
 // ---------------------------------------------------------------- slice select
@@ -114,6 +127,10 @@ struct SliceDesc {
   int64_t* leaf_off;              // out: per-leaf dynamic element offset
   int64_t* counter;               // in/out: current slice index (incremented)
   unsigned* absmax; int32_t absmax_first, absmax_count;  // zeroed per slice
+  // delayed scaling of fused plane outputs: hist[s] = running max over finished slices
+  // of step s's output absmax (merged here from the absmax slot before it is zeroed);
+  // pexp[s] = 11 - e(hist[s]) puts the largest value seen so far near 2^11 (32x margin)
+  unsigned* hist; int* pexp;
 };
 
 // kernel launchers (kernels.cu / gemm_tcgen05.cu)
@@ -133,6 +150,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t
 // one B slab per 256-row tile (not a grouped merge)
 bool gemm_pair_ok(const GemmArgs& a, int min_m);
 int gemm_pair_min_m();                   // reads TN_GEMM_PAIR_MIN_M
+int gemm_epi_warps();                    // reads TN_GEMM_EPI (8 or 16)
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
                       int planes, int box_rows, char* err, size_t errcap);
 

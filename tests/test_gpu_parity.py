@@ -146,6 +146,8 @@ ROUTES = {
                         "TN_PREP_FORCE": "2"},
     "tc_prep_bitperm": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8",
                         "TN_PREP_FORCE": "4"},
+    "tc_unfused": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                   "TN_FUSE_PLANES": "0"},
     "tc_grouped": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                    "TN_GROUP": "2"},
     "tc_pair": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
@@ -178,7 +180,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
     if route == "tc":
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
-        assert any(s["out_gen"] for s in c.plan_json()["steps"])
+        steps = c.plan_json()["steps"]
+        assert any(s["out_gen"] for s in steps)
+        if mode != "single":     # a producer epilogue writes its consumer's fp16 planes
+            assert any(s["planes_out"] for s in steps)
     if route == "tc_grouped" and mode == "sparse":
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
