@@ -295,7 +295,22 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       // completion bytes of both CTAs go to the leader's full barrier
       int stage = 0;
       uint32_t phase = 0;
+      unsigned long long target = 0;
+      const int per_unit = PAIR ? 2 : 1;
       for (int64_t tile = unit; tile < args.n_tiles; tile += units) {
+        if (args.wave_sync) {
+          // wave w = tile / units: producers with a tile in it = per_unit * min(units, rest)
+          const int64_t w0 = tile - unit;
+          const int64_t rest = args.n_tiles - w0;
+          target += (unsigned long long)(per_unit * (rest < units ? rest : units));
+          atomicAdd(args.wave_ctr, 1ull);
+          for (int spin = 0; spin < 20000; ++spin) {   // bounded: a locality hint, never a hang
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(args.wave_ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+          }
+        }
         int j, mt, nt;
         decode_tile(args, tile, j, mt, nt);
         const int sa = args.ia ? args.ia[j] : 0;
@@ -684,6 +699,29 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
     p.tiles_m = (a.M + 2 * BM - 1) / (2 * BM);
     p.n_tiles = (int64_t)p.tiles_m * p.tiles_n * a.J;
     int64_t pairs = p.n_tiles < num_sms / 2 ? p.n_tiles : num_sms / 2;
+    // a persistent grid must be co-resident (the wave sync waits on every producer):
+    // never launch more clusters than can be active at once
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3((unsigned)num_sms);
+      q.blockDim = dim3(64 + 32 * EW);
+      q.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 2;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, cgemm_tcgen05_kernel<PASSES, EW, PAIR>, &q) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = num_sms / 2;
+      }
+      max_clusters = n;
+    }
+    if (pairs > max_clusters) pairs = max_clusters;
     if (pairs < 1) pairs = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * pairs));
@@ -750,6 +788,10 @@ bool gemm_pair_ok(const GemmArgs& a, int min_m) {
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s) {
+  if (a.wave_sync) {
+    cudaError_t e = cudaMemsetAsync(a.wave_ctr, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+  }
   if (a.use_pair)
     return passes == 3 ? launch_impl<3, 8, true>(a, num_sms, s) : launch_impl<1, 8, true>(a, num_sms, s);
   if (gemm_epi_warps() == 16)

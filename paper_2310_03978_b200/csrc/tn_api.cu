@@ -187,6 +187,7 @@ struct tn_ctx {
   unsigned* d_hist = nullptr;      // delayed scaling: running output absmax per step
   int* d_pexp = nullptr;           // delayed scaling: exponent per step (slice_select)
   int* d_flag = nullptr;           // fused plane overflow flag
+  unsigned long long* d_wave = nullptr;   // GEMM wave-sync counter
   int64_t* d_gt = nullptr;         // general-transposer tile tables
   int64_t device_bytes = 0;
   // profiling
@@ -229,7 +230,7 @@ void free_dev(tn_ctx* c) {
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
                   c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt,
-                  c->d_hist, c->d_pexp, c->d_flag};
+                  c->d_hist, c->d_pexp, c->d_flag, c->d_wave};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
@@ -238,7 +239,7 @@ void free_dev(tn_ctx* c) {
   c->d_einsum = nullptr; c->d_prep = nullptr; c->d_one = nullptr;
   c->d_partial = nullptr;
   c->d_gt = nullptr;
-  c->d_hist = nullptr; c->d_pexp = nullptr; c->d_flag = nullptr;
+  c->d_hist = nullptr; c->d_pexp = nullptr; c->d_flag = nullptr; c->d_wave = nullptr;
   c->planned = false;
 }
 
@@ -611,6 +612,7 @@ tn_status build_plan(tn_ctx* c) {
   const int pair_min_m = tn::gemm_pair_min_m();            // CTA-pair GEMM for M >= this
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
+  const int wave_sync = env_int("TN_WAVE_SYNC", 1);        // GEMM wave synchronisation (L2 reuse)
                                                            // (2: column-contiguous case only)
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
@@ -1041,6 +1043,7 @@ tn_status build_plan(tn_ctx* c) {
   if ((st = dev_alloc(c, &c->d_hist, (size_t)n_steps))) return st;
   if ((st = dev_alloc(c, &c->d_pexp, (size_t)n_steps))) return st;
   if ((st = dev_alloc(c, &c->d_flag, 1))) return st;
+  if ((st = dev_alloc(c, &c->d_wave, 1))) return st;
   TN_CUDA(cudaMemsetAsync(c->d_hist, 0, n_steps * sizeof(unsigned), sm));
   TN_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), sm));
   if (!tables.empty())
@@ -1369,6 +1372,8 @@ tn_status build_plan(tn_ctx* c) {
         g.n_tiles = (int64_t)g.tiles_m * g.tiles_n;
       }
       g.use_pair = tn::gemm_pair_ok(g, pair_min_m) ? 1 : 0;
+      g.wave_ctr = c->d_wave;
+      g.wave_sync = (wave_sync && sp.k >= 1024) ? 1 : 0;
       g.out_gen = sp.out_gen ? 1 : 0;
       if (sp.out_gen) {
         auto lg = [](int64_t x) { int q = 0; while ((int64_t(1) << q) < x) ++q; return q; };
@@ -2209,6 +2214,9 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     g.kchunk = passes == 3 ? c->kchunk3 : c->kchunk1;
     g.group_m = c->group_m;
     g.use_pair = tn::gemm_pair_ok(g, tn::gemm_pair_min_m()) ? 1 : 0;
+    if (!c->d_wave) TN_CUDA(cudaMalloc(&c->d_wave, sizeof(unsigned long long)));
+    g.wave_ctr = c->d_wave;
+    g.wave_sync = (env_int("TN_WAVE_SYNC", 1) && k >= 1024) ? 1 : 0;
     {
       Timer tm(c, 0, 8.0 * (double)J * m * n * k, 8.0 * (double)(ga * m * k + gb * n * k + J * m * n));
       TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));

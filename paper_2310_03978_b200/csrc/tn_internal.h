@@ -115,6 +115,12 @@ struct GemmArgs {
   int* plane_scale_out;
   const int* plane_pexp;          // delayed-scaling exponent (SliceDesc.pexp[step])
   int* overflow;                  // set when a plane value reaches the fp16 range limit
+  // wave synchronisation (locality hint): before each tile every producer arrives on a
+  // global counter and waits (bounded spin) until all producers of the wave have
+  // arrived, so the tiles that share A / B panels stream the same k-blocks together
+  // and the panels are read from L2 instead of DRAM; zeroed per launch
+  unsigned long long* wave_ctr;
+  int32_t wave_sync, pad_w;
 };
 
 // ---------------------------------------------------------------- slice select
