@@ -469,20 +469,24 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       float sr[WC], si[WC];
 #pragma unroll
       for (int i = 0; i < WC; ++i) { sr[i] = 0.f; si[i] = 0.f; }
+      // column half entirely beyond N (narrow GEMMs): nothing to drain, only release
+      const bool cols_live = (int)(nt * BN + half * WC) < args.N;
       for (int ch = 0; ch < nchunks; ++ch) {
         mbar_wait(&cfull[cb], cphase);
         fence_after();
         const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + cb * 256 + half * WC;
+        if (cols_live) {
 #pragma unroll
-        for (int c = 0; c < WC / 32; ++c) {
-          uint32_t vr[32], vi[32];
-          TN_LD32(vr, tb + c * 32);
-          TN_LD32(vi, tb + 128 + c * 32);
-          tmem_wait_ld();
+          for (int c = 0; c < WC / 32; ++c) {
+            uint32_t vr[32], vi[32];
+            TN_LD32(vr, tb + c * 32);
+            TN_LD32(vi, tb + 128 + c * 32);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {     // fp32 round-to-nearest promotion of the chunk
-            sr[c * 32 + i] += __uint_as_float(vr[i]);
-            si[c * 32 + i] += __uint_as_float(vi[i]);
+            for (int i = 0; i < 32; ++i) {     // fp32 round-to-nearest promotion of the chunk
+              sr[c * 32 + i] += __uint_as_float(vr[i]);
+              si[c * 32 + i] += __uint_as_float(vi[i]);
+            }
           }
         }
         fence_before();
