@@ -36,7 +36,7 @@
 //               and hands finished chunks to the epilogue.
 //   warps 2-9   epilogue: warp (quadrant q, half h) owns TMEM lanes 32q..32q+31
 //               and output columns 64h..64h+63 of both Cr and Ci; tcgen05.ld
-//               32x32b.x32 -> fp32 RN register sums -> at tile end scale by
+//               32x32b.x32 -> fp32 RN register sums of the chunks scaled by
 //               2^-(sA+sB) and store complex64 (or fused fp64 accumulate into the
 //               slice sum, a8) + absmax of the result for the consumer's rescale.
 #include "tn_internal.h"
@@ -454,7 +454,6 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       const int sab = *args.scaleA + *args.scaleB;
       plane_sc = max(sab + args.plane_exp, *args.plane_pexp);
       if (blockIdx.x == 0 && threadIdx.x == 64) *args.plane_scale_out = plane_sc;
-      plane_sc -= sab;
     }
     bool plane_ovf = false;
     float amax = 0.f;
@@ -483,9 +482,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
             TN_LD32(vi, tb + 128 + c * 32);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {     // fp32 round-to-nearest promotion of the chunk
-              sr[c * 32 + i] += __uint_as_float(vr[i]);
-              si[c * 32 + i] += __uint_as_float(vi[i]);
+            for (int i = 0; i < 32; ++i) {     // fp32 round-to-nearest promotion of the chunk,
+              // with the power-of-two output scale folded in (exact: commutes with RN)
+              sr[c * 32 + i] = fmaf(__uint_as_float(vr[i]), scale, sr[c * 32 + i]);
+              si[c * 32 + i] = fmaf(__uint_as_float(vi[i]), scale, si[c * 32 + i]);
             }
           }
         }
@@ -605,14 +605,25 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
           }
           const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff;
           const int64_t* tc = tab + half * WC;
+          if (args.cols_contig && n0 + WC <= args.N) {
+            // the 64 columns are one contiguous, 16-B aligned output run
+            float4* dst = reinterpret_cast<float4*>(args.C + rb + tc[0]);
+#pragma unroll
+            for (int i = 0; i < WC / 2; ++i) {
+              const float r0 = sr[2 * i], i0 = si[2 * i], r1 = sr[2 * i + 1], i1 = si[2 * i + 1];
+              dst[i] = make_float4(r0, i0, r1, i1);
+              amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
+            }
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < WC; i += 2) {      // full unroll: sr/si stay in registers
             if (n0 + i >= args.N) continue;
-            const float r0 = sr[i] * scale, i0 = si[i] * scale;
+            const float r0 = sr[i], i0 = si[i];
             const int64_t a0 = rb + tc[i];
             amax = fmaxf(amax, fmaxf(fabsf(r0), fabsf(i0)));
             if (n0 + i + 1 < args.N) {
-              const float r1 = sr[i + 1] * scale, i1 = si[i + 1] * scale;
+              const float r1 = sr[i + 1], i1 = si[i + 1];
               const int64_t a1 = rb + tc[i + 1];
               amax = fmaxf(amax, fmaxf(fabsf(r1), fabsf(i1)));
               if (a1 == a0 + 1 && (a0 & 1) == 0) {
@@ -636,7 +647,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
 #pragma unroll
           for (int i = 0; i < WC; ++i) {
             if (n0 + i < args.N) {
-              const float re = sr[i] * scale, im = si[i] * scale;
+              const float re = sr[i], im = si[i];
               double2 o = args.acc[base + i];
               o.x += (double)re;
               o.y += (double)im;
@@ -648,8 +659,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
           float4* dst = reinterpret_cast<float4*>(args.C + base);
 #pragma unroll
           for (int i = 0; i < WC / 2; ++i) {
-            const float r0 = sr[2 * i] * scale, i0 = si[2 * i] * scale;
-            const float r1 = sr[2 * i + 1] * scale, i1 = si[2 * i + 1] * scale;
+            const float r0 = sr[2 * i], i0 = si[2 * i];
+            const float r1 = sr[2 * i + 1], i1 = si[2 * i + 1];
             dst[i] = make_float4(r0, i0, r1, i1);
             amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
           }
@@ -657,7 +668,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
 #pragma unroll
           for (int i = 0; i < WC; ++i) {
             if (n0 + i < args.N) {
-              const float re = sr[i] * scale, im = si[i] * scale;
+              const float re = sr[i], im = si[i];
               args.C[base + i] = make_float2(re, im);
               amax = fmaxf(amax, fmaxf(fabsf(re), fabsf(im)));
             }
@@ -666,7 +677,6 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       }
     }
     if (args.out_planes) {
-      amax *= scale;       // raw accumulator maxima -> true values (absmax_out below)
       if (__any_sync(0xffffffffu, plane_ovf) && lane == 0) atomicOr(args.overflow, 1);
     }
     if (args.absmax_out) {

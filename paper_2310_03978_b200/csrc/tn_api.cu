@@ -1381,6 +1381,7 @@ tn_status build_plan(tn_ctx* c) {
         g.n_qo = (int32_t)sp.qo.size();
         for (int q = 0; q < g.n_po; ++q) { g.po_sh[q] = (uint8_t)lg(sp.po[q].ext); g.po_str[q] = sp.po[q].stride; }
         for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)lg(sp.qo[q].ext); g.qo_str[q] = sp.qo[q].stride; }
+        g.cols_contig = (g.n_qo > 0 && g.qo_str[g.n_qo - 1] == 1 && g.qo_sh[g.n_qo - 1] >= 6) ? 1 : 0;
       }
     }
     live.erase(sp.j);
@@ -1479,6 +1480,7 @@ tn_status build_plan(tn_ctx* c) {
         g.n_qo = (int)qo.size();
         for (int q = 0; q < g.n_po; ++q) { g.po_sh[q] = (uint8_t)po[q].first; g.po_str[q] = po[q].second; }
         for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)qo[q].first; g.qo_str[q] = qo[q].second; }
+        g.cols_contig = 0;   // plane mode has its own 8-column vectors
         int lk = 0;
         while ((int64_t(1) << lk) < pp.k) ++lk;
         g.plane_exp = -16 - lk;

@@ -99,7 +99,8 @@ struct GemmArgs {
   // with row m / column n decomposed over power-of-two extents (log2 in po_sh / qo_sh,
   // outer -> inner).  Lets the producer write the consumer's preferred layout
   // ([P keep][Q keep][contracted, sorted]) so the consumer's operand is K-contiguous.
-  int32_t out_gen, n_po, n_qo, pad_o;
+  int32_t out_gen, n_po, n_qo;
+  int32_t cols_contig;            // out_gen: the 64 columns of a warp are one contiguous run
   uint8_t po_sh[16], qo_sh[16];
   int64_t po_str[16], qo_str[16];
   // fused consumer prep (a3 + a6 in this epilogue): the output is written directly as the
