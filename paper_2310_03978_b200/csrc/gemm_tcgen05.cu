@@ -639,6 +639,41 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
         }
         continue;
       }
+      if (args.pair_map) {
+        // ---- dense merge: keep the (slab a, slab b) blocks that are merged configurations
+        if (m < args.M && n0 < args.N) {
+          const int a = m >> args.pm_sh_m, p = m & ((1 << args.pm_sh_m) - 1);
+          const int shn = args.pm_sh_n, R1 = 1 << shn;
+          const int32_t* pm = args.pair_map + (int64_t)a * args.pm_g1;
+          const int64_t prow = (int64_t)p << shn;
+          int bprev = -1, jj = -1;
+#pragma unroll
+          for (int i = 0; i < WC; i += 2) {
+            const int n = n0 + i;
+            if (n >= args.N) continue;
+            if (shn >= 1) {                 // columns n, n+1 belong to the same slab b
+              const int b = n >> shn;
+              if (b != bprev) { jj = pm[b]; bprev = b; }
+              if (jj < 0) continue;
+              const int64_t addr = ((int64_t)jj << (args.pm_sh_m + shn)) + prow + (n & (R1 - 1));
+              const float r0 = sr[i], i0 = si[i], r1 = sr[i + 1], i1 = si[i + 1];
+              *reinterpret_cast<float4*>(args.C + addr) = make_float4(r0, i0, r1, i1);
+              amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
+            } else {                        // one column per slab
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (n + u >= args.N) continue;
+                const int32_t ju = pm[n + u];
+                if (ju < 0) continue;
+                const int64_t addr = ((int64_t)ju << args.pm_sh_m) + p;
+                args.C[addr] = make_float2(sr[i + u], si[i + u]);
+                amax = fmaxf(amax, fmaxf(fabsf(sr[i + u]), fabsf(si[i + u])));
+              }
+            }
+          }
+        }
+        continue;
+      }
       int64_t orow = (int64_t)j * args.M + m;
       if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
       if (m < args.M && n0 < args.N && orow >= 0) {

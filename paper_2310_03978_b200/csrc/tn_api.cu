@@ -86,6 +86,12 @@ struct StepPlan {
   // slab-grouped merge (tensor cores): the P side's rows are gathered (j, q) rows sorted
   // by the Q side's slab, each slab group padded to 128 rows; see DESIGN.md "Sparse merges"
   bool grouped = false;
+  // dense merge: an Eq. 7 merge whose pairs (slabA(j), slabB(j)) cover most of the slab
+  // product runs as ONE dense GEMM over [slabA rows] x [slabB rows] and the epilogue keeps
+  // the pairs that exist (pair_map[a][b] = j, -1 = dropped); DESIGN.md "Sparse merges"
+  bool dense_merge = false;
+  std::vector<int32_t> pair_map;
+  int64_t pair_off = -1;
   int64_t g_rows = 0;           // gathered rows (multiple of 128)
   std::vector<int32_t> g_rowmap, g_blk;   // output row of each gathered row; Q slab per block
   int64_t g_rowmap_off = -1, g_blk_off = -1;
@@ -612,6 +618,7 @@ tn_status build_plan(tn_ctx* c) {
   const int pair_min_m = tn::gemm_pair_min_m();            // CTA-pair GEMM for M >= this
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
+  const int dense_mode = env_int("TN_DENSE_MERGE", 1);     // 0 off, 1 cost rule, 2 always (tests)
   const int wave_sync = env_int("TN_WAVE_SYNC", 1);        // GEMM wave synchronisation (L2 reuse)
                                                            // (2: column-contiguous case only)
   const int n_leaves = c->n_tensors;
@@ -813,6 +820,25 @@ tn_status build_plan(tn_ctx* c) {
         }
       }
     }
+    if (sp.merge && sp.J > 1 && !sp.grouped && dense_mode > 0 && !disable_tc && !sp.final_step &&
+        sp.k >= tc_k && sp.k < INT32_MAX) {
+      auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+      const double slabs = (double)gA.ext * (double)gB.ext;
+      const bool narrow = !sp.tc || std::min(sp.m, sp.n) < 128;   // batched tiles mostly padding
+      if ((dense_mode == 2 || (narrow && (double)sp.J >= 0.5 * slabs)) && p2(sp.m) && p2(sp.n) &&
+          gA.ext * sp.m < INT32_MAX && gB.ext * sp.n < INT32_MAX && slabs < 1e8 &&
+          (dense_mode == 2 || std::max(gA.ext * sp.m, gB.ext * sp.n) >= 128)) {
+        sp.dense_merge = true;
+        sp.tc = true;
+        sp.swap = gB.ext * sp.n > gA.ext * sp.m;   // M side = the larger dense extent
+        const int64_t G0 = sp.swap ? gB.ext : gA.ext, G1 = sp.swap ? gA.ext : gB.ext;
+        sp.pair_map.assign((size_t)(G0 * G1), -1);
+        for (int64_t j = 0; j < sp.J; ++j) {
+          const int64_t s0 = sp.swap ? sp.ib[j] : sp.ia[j], s1 = sp.swap ? sp.ia[j] : sp.ib[j];
+          sp.pair_map[s0 * G1 + s1] = (int32_t)j;
+        }
+      }
+    }
 
     // output layout: [J][P dims][Q dims], P = A side unless swapped
     // SIMT mode (see kernels.cu): 2 = split-K dot, 1 = skinny (one small operand)
@@ -890,7 +916,7 @@ tn_status build_plan(tn_ctx* c) {
       // by label]: the consumer's operand is then K-contiguous in the canonical (sorted)
       // K order, so its prep is a streaming copy instead of a transpose
       auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
-      bool gen = sp.tc && !sp.grouped && out_layout && !kc.empty();
+      bool gen = sp.tc && !sp.grouped && !sp.dense_merge && out_layout && !kc.empty();
       for (auto& d : P) gen = gen && p2(d.ext);
       for (auto& d : Q) gen = gen && p2(d.ext);
       if (gen) {
@@ -957,6 +983,10 @@ tn_status build_plan(tn_ctx* c) {
       tables.insert(tables.end(), sp.ia.begin(), sp.ia.end());
       sp.ib_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.ib.begin(), sp.ib.end());
+    }
+    if (sp.dense_merge) {
+      sp.pair_off = (int64_t)tables.size();
+      tables.insert(tables.end(), sp.pair_map.begin(), sp.pair_map.end());
     }
     if (sp.grouped) {
       sp.g_rowmap_off = (int64_t)tables.size();
@@ -1329,10 +1359,12 @@ tn_status build_plan(tn_ctx* c) {
         sp.prep_total[side] = p.plane_elems;
         CUtensorMap* map = side == 0 ? &sp.gemm.mapA : &sp.gemm.mapB;
         if (!c->host_only &&
-            (!tn::encode_plane_map(map, p.dst, sp.Kpad, sp.R[side], sp.G[side], 4, 128, errbuf,
-                                   sizeof(errbuf)) ||
-             (side == 1 && !tn::encode_plane_map(&sp.gemm.mapB2, p.dst, sp.Kpad, sp.R[side],
-                                                 sp.G[side], 4, 64, errbuf, sizeof(errbuf)))))
+            (!tn::encode_plane_map(map, p.dst, sp.Kpad, sp.dense_merge ? sp.G[side] * sp.R[side] : sp.R[side],
+                                   sp.dense_merge ? 1 : sp.G[side], 4, 128, errbuf, sizeof(errbuf)) ||
+             (side == 1 && !tn::encode_plane_map(&sp.gemm.mapB2, p.dst, sp.Kpad,
+                                                 sp.dense_merge ? sp.G[side] * sp.R[side] : sp.R[side],
+                                                 sp.dense_merge ? 1 : sp.G[side], 4, 64, errbuf,
+                                                 sizeof(errbuf)))))
           return fail(TN_ERR_INTERNAL, errbuf);
         if (c->debug_plan) {
           fprintf(stderr, "[tn] step %d prep%c G=%lld R=%lld K=%lld kind=%d T=%d rows:", s,
@@ -1363,6 +1395,23 @@ tn_status build_plan(tn_ctx* c) {
       g.blk_slab_b = nullptr;
       g.rowmap = nullptr;
       g.use_pair = 0;
+      if (sp.dense_merge) {   // one dense GEMM over the slab product, pair-mapped epilogue
+        g.J = 1;
+        g.ia = nullptr;
+        g.ib = nullptr;
+        g.M = (int32_t)(sp.G[0] * sp.R[0]);
+        g.N = (int32_t)(sp.G[1] * sp.R[1]);
+        g.tiles_m = (g.M + 127) / 128;
+        g.tiles_n = (g.N + 127) / 128;
+        g.n_tiles = (int64_t)g.tiles_m * g.tiles_n;
+        g.pair_map = c->d_tables + sp.pair_off;
+        int lm = 0, ln = 0;
+        while ((int64_t(1) << lm) < sp.R[0]) ++lm;
+        while ((int64_t(1) << ln) < sp.R[1]) ++ln;
+        g.pm_sh_m = lm;
+        g.pm_sh_n = ln;
+        g.pm_g1 = (int32_t)sp.G[1];
+      }
       if (sp.grouped) {   // one GEMM over the gathered rows; X slab per 128-row block
         g.J = 1;
         g.ia = nullptr;
@@ -1397,12 +1446,12 @@ tn_status build_plan(tn_ctx* c) {
   if (fuse_planes)
     for (int s = 0; s < n_steps; ++s) {
       StepPlan& cs = c->steps[s];
-      if (!cs.tc || cs.grouped) continue;
+      if (!cs.tc || cs.grouped || cs.dense_merge) continue;
       for (int side = 0; side < 2; ++side) {
         const int ps = side_producer[s][side];
         if (ps < 0) continue;
         StepPlan& pp = c->steps[ps];
-        if (!pp.tc || pp.grouped || pp.final_step || pp.planes_consumer >= 0) continue;
+        if (!pp.tc || pp.grouped || pp.dense_merge || pp.final_step || pp.planes_consumer >= 0) continue;
         if (c->debug_plan) fprintf(stderr, "[tn] fuse candidate %d->%d side %d\n", ps, s, side);
         const tn::PrepDesc& pd = pds[cs.prep_idx + side];
         const int64_t Kp = cs.Kpad;
@@ -2041,12 +2090,13 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
              sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false",
              sp.tc ? (sp.skip_prep[0] ? -1 : sp.r_fast[0]) : -1,
-             sp.tc ? (sp.skip_prep[1] ? -1 : sp.r_fast[1]) : -1, sp.planes_consumer >= 0 ? "true" : "false");
+             sp.tc ? (sp.skip_prep[1] ? -1 : sp.r_fast[1]) : -1, sp.planes_consumer >= 0 ? "true" : "false",
+             sp.dense_merge ? "true" : "false");
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";

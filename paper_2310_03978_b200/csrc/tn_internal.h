@@ -122,6 +122,10 @@ struct GemmArgs {
   // and the panels are read from L2 instead of DRAM; zeroed per launch
   unsigned long long* wave_ctr;
   int32_t wave_sync, pad_w;
+  // dense merge (pair-mapped epilogue): row = a*2^pm_sh_m + p, col = b*2^pm_sh_n + q,
+  // j = pair_map[a*pm_g1 + b] (-1: not a merged configuration), out C[j][p][q]
+  const int32_t* pair_map;
+  int32_t pm_sh_m, pm_sh_n, pm_g1, pad_pm;
 };
 
 // ---------------------------------------------------------------- slice select

@@ -148,6 +148,8 @@ ROUTES = {
                         "TN_PREP_FORCE": "4"},
     "tc_unfused": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
                    "TN_FUSE_PLANES": "0"},
+    "tc_dense_merge": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
+                       "TN_GROUP": "0", "TN_DENSE_MERGE": "2"},
     "tc_grouped": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                    "TN_GROUP": "2"},
     "tc_pair": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
@@ -184,6 +186,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
         assert any(s["out_gen"] for s in steps)
         if mode != "single":     # a producer epilogue writes its consumer's fp16 planes
             assert any(s["planes_out"] for s in steps)
+    if route == "tc_dense_merge" and mode == "sparse":
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        assert any(s["dense_merge"] for s in c.plan_json()["steps"])
     if route == "tc_grouped" and mode == "sparse":
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
@@ -318,6 +324,30 @@ def test_c3_sparse_state_sampled_subnetwork(ctx):
           f"max J {maxJ}, rel_l2 {err:.3e}")
     assert maxJ > 1000
     assert any(s["grouped"] for s in pj["steps"])
+    assert err <= EXT_TOL
+
+
+@pytest.mark.timeout(900)
+def test_c4_sparse_state_sampled_subnetwork(ctx):
+    """Sycamore-53 m=18 with a 2^16-sample sparse-state boundary (the bench's
+    `--boundary sparse16` order): one slice of a sub-network (extra bonds fixed) vs the
+    oracle over all 2^16 amplitudes; the plan's dense slab-product merge (J ~ GA*GB)
+    and gather-batched merges run at full width."""
+    from tnworkloads.network import fix_bonds
+    w = configs.c4("sparse16")
+    fine, pc = _refine(w, 2e11)
+    extra = fine[len(w.sliced):]
+    sub = fix_bonds(w.net, {x: 0 for x in extra})
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(sub, w.samples, w.path, w.sliced)
+    pj = c.plan_json()
+    c.contract(0, 1)
+    got = c.sum_slices_host()
+    c.close()
+    ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
+    err = rel_l2(got, ref)
+    print(f"C4 sparse16 sub-network: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
+          f"dense merges {sum(s['dense_merge'] for s in pj['steps'])}, rel_l2 {err:.3e}")
     assert err <= EXT_TOL
 
 
