@@ -459,6 +459,120 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
   }
 }
 
+// ---------------------------------------------------------------- operand prep, gate-folded
+// The operand is out[o][n][v] = Σ_k Y[n][k] X[o, v, k] of a skinny SIMT step that is not
+// run: a tile loads the X values of its carry bits (dest bits other than n) for every k,
+// and each plane element applies the small matrix Y (staged in smem) while it is
+// written.  Saves the skinny step's full pass over the big tensor.  Scale: |out| <=
+// 2 K absmax(X) absmax(Y) per real component (bound, no absmax of out exists).
+constexpr int GP_TMAX = 4096;
+constexpr int GP_KMAX = 16, GP_NMAX = 256;
+constexpr size_t GP_SMEM = GP_TMAX * 8 /*in*/ + GP_TMAX * 8 /*out*/ + 1024 * 8 /*Y*/ + 128 * 8 /*src*/ +
+                           GP_TMAX / 8 * 8 /*dst*/ + GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
+
+template <int PLANES>
+__global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __restrict__ gd,
+                                                           const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  float2* tin = reinterpret_cast<float2*>(dyn);                     // [TS] X values (carry, k)
+  float2* tout = tin + GP_TMAX;                                      // [TD] outputs, dest order
+  float2* Ys = tout + GP_TMAX;                                       // [N][K]
+  int64_t* s_src = reinterpret_cast<int64_t*>(Ys + 1024);            // [128]
+  int64_t* s_dst = s_src + 128;                                      // [TD/8]
+  uint16_t* s_fc = reinterpret_cast<uint16_t*>(s_dst + GP_TMAX / 8); // [2^cb] f of carry pos
+  uint16_t* s_fn = s_fc + GP_TMAX;                                   // [N] f of n index
+  const int TD = 1 << d.bp_t, TS = 1 << d.g_ts, K = d.g_K, N = d.g_N, CB = 1 << d.g_cbits;
+  {
+    const int64_t* tab = d.bp_tab;
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) s_src[i] = tab[i];
+    for (int i = threadIdx.x; i < TD / 8; i += blockDim.x) s_dst[i] = tab[128 + i];
+    const uint16_t* fc = reinterpret_cast<const uint16_t*>(tab + 128 + TD / 8);
+    for (int i = threadIdx.x; i < CB; i += blockDim.x) s_fc[i] = fc[i];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_fn[i] = fc[GP_TMAX + i];
+    const float2* Y = d.gy + d.gy_off + (d.gy_leaf >= 0 ? leaf_off[d.gy_leaf] : 0);
+    for (int e = threadIdx.x; e < N * K; e += blockDim.x) {
+      const int n = e / K, k = e % K;
+      Ys[e] = Y[decompose(n, d.g_nn, d.gy_n_ext, d.gy_n_s) + decompose(k, d.g_nk, d.gy_k_ext, d.gy_k_s)];
+    }
+  }
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  float scale;
+  {
+    const float bound = 2.f * (float)K * __uint_as_float(*d.absmax_in) * __uint_as_float(*d.absmax_y);
+    int s = 0;
+    if (bound > 0.f) {
+      int e;
+      frexpf(bound, &e);
+      s = max(-120, min(120, 15 - e));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *d.scale_out = s;
+    scale = ldexpf(1.0f, s);
+  }
+  const bool vec = d.bp_vec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
+    int64_t sc = 0, dc = 0;
+    for (int i = 0; i < d.nc; ++i)
+      if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
+    __syncthreads();   // tables / Y ready, previous tile consumed
+    const float2* sp = src + sc;
+    if (vec) {           // e, e+1 adjacent in X: 16-B loads
+      float4 v[GP_TMAX / 512];
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < TS) v[i] = __ldg(reinterpret_cast<const float4*>(sp + s_src[e & 63] + s_src[64 + (e >> 6)]));
+      }
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < TS) *reinterpret_cast<float4*>(tin + e) = v[i];
+      }
+    } else {
+      float2 v[GP_TMAX / 256];
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 256; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < TS) v[i] = __ldg(sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+      }
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 256; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < TS) tin[e] = v[i];
+      }
+    }
+    __syncthreads();
+    // one thread per carry position: its K X values in registers, all N outputs
+    for (int cp = threadIdx.x; cp < CB; cp += blockDim.x) {
+      float2 x[GP_KMAX];
+#pragma unroll
+      for (int k = 0; k < GP_KMAX; ++k) x[k] = k < K ? tin[cp + k * CB] : make_float2(0.f, 0.f);
+      const int fcp = s_fc[cp];
+      for (int n = 0; n < N; ++n) {
+        const float2* yr = Ys + n * K;
+        float ar = 0.f, ai = 0.f;
+#pragma unroll
+        for (int k = 0; k < GP_KMAX; ++k) {
+          if (k < K) {
+            const float2 y = yr[k];
+            ar = fmaf(x[k].x, y.x, fmaf(-x[k].y, y.y, ar));
+            ai = fmaf(x[k].x, y.y, fmaf(x[k].y, y.x, ai));
+          }
+        }
+        tout[fcp + s_fn[n]] = make_float2(ar, ai);
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
+      float2 o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = tout[8 * q + j];
+      split_store8<PLANES>(d, dc + s_dst[q], o, scale);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- SIMT einsum, general
 // One thread per output C[j][m][n]; fp64 accumulation (a long fp32 RN chain would
 // cost ~2^-24·sqrt(K/2) relative).
@@ -998,6 +1112,21 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
                         const int64_t* leaf_off, cudaStream_t s) {
   const int th = 256;
+  if (kind == 5) {   // gate-folded prep
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(prep_gate_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
+      cudaFuncSetAttribute(prep_gate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
+      attr = true;
+    }
+    const int64_t tiles = total / std::max(tile_T, 1);
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 2);
+    if (planes == 4)
+      prep_gate_kernel<4><<<g, th, GP_SMEM, s>>>(d_desc, leaf_off);
+    else
+      prep_gate_kernel<2><<<g, th, GP_SMEM, s>>>(d_desc, leaf_off);
+    return cudaGetLastError();
+  }
   if (kind == 4) {   // bit-permutation transposer, tiles of tile_T <= 4096 elements
     static bool attr = false;
     if (!attr) {

@@ -90,6 +90,11 @@ struct StepPlan {
   // product runs as ONE dense GEMM over [slabA rows] x [slabB rows] and the epilogue keeps
   // the pairs that exist (pair_map[a][b] = j, -1 = dropped); DESIGN.md "Sparse merges"
   bool dense_merge = false;
+  // gate folding: this skinny SIMT step is not launched;
+  // its tensor-core consumer's prep applies it while transposing (x_slot / y_slot: absmax
+  // slots of its big and small operands)
+  bool folded = false;
+  int x_slot = -1, y_slot = -1;
   std::vector<int32_t> pair_map;
   int64_t pair_off = -1;
   int64_t g_rows = 0;           // gathered rows (multiple of 128)
@@ -169,6 +174,9 @@ struct tn_ctx {
   // plan
   std::vector<StepPlan> steps;
   View root;
+  // gate folding decided by a previous planning pass: the folded step's output is not
+  // allocated and its inputs stay live until its consumer's prep has read them
+  std::vector<char> fold_hint;
   std::vector<int32_t> out_pos;
   int64_t n_out = 0, acc_elems = 1;
   double flops_per_slice = 0, tc_flops = 0, bytes_per_slice = 0, peak = 0;
@@ -421,6 +429,160 @@ bool plan_bp(tn::PrepDesc& p, std::vector<int64_t>& tab) {
   return true;
 }
 
+// Gate-folded prep plan (prep kind 5, kernels.cu prep_gate_kernel).  The operand is
+// the output out[o][n][v] (contiguous [Xo][N][V]) of the skinny SIMT step `e`; each
+// plane-layout bit is a carry bit (an o or v bit: an X weight) or an n bit.  The tile
+// holds every n bit, the plane vectors' 3 lowest destination bits and the carry bits of
+// smallest X weight; the source tile is its carry bits plus all k bits.
+bool plan_gate(tn::PrepDesc& p, const tn::EinsumDesc& e, std::vector<int64_t>& tab) {
+  auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+  auto lg = [](int64_t x) { int q = 0; while ((int64_t(1) << q) < x) ++q; return q; };
+  if (p.Kpad != p.K || p.K < 8 || !p2(p.K) || !p2(p.R) || p.G != 1 || p.rowoff) return false;
+  if (e.mode != 1 || e.J != 1 || e.acc || !p2(e.N) || !p2(e.K) || !p2(e.V) || !p2(e.M)) return false;
+  if (e.N * e.K > 1024 || e.N > 256 || e.K > 16 || e.nn > 8 || e.nk > 8) return false;
+  const int lv = lg(e.V), ln = lg(e.N), lk = lg(e.K), lo = lg(e.M / e.V);
+  // X weight of each o-index bit (Xo dims, outer -> inner in m_ext / m_sa [0, nm-1))
+  std::vector<int64_t> ow;
+  for (int d = e.nm - 2; d >= 0; --d) {
+    if (!p2(e.m_ext[d])) return false;
+    for (int64_t t = 1; t < e.m_ext[d]; t <<= 1) ow.push_back(e.m_sa[d] * t);
+  }
+  if ((int)ow.size() != lo) return false;
+  const int64_t vs = e.m_sa[e.nm - 1];
+  std::vector<int64_t> kw;                         // X weight of each k-index bit
+  for (int d = e.nk - 1; d >= 0; --d) {
+    if (!p2(e.k_ext[d])) return false;
+    for (int64_t t = 1; t < e.k_ext[d]; t <<= 1) kw.push_back(e.k_sa[d] * t);
+  }
+  if ((int)kw.size() != lk) return false;
+  // destination bits -> S-output weights (as in plan_bp)
+  std::vector<int64_t> ws;
+  for (int d = p.nk - 1; d >= 0; --d) {
+    if (!p2(p.k_ext[d])) return false;
+    for (int64_t t = 1; t < p.k_ext[d]; t <<= 1) ws.push_back(t * p.k_s[d]);
+  }
+  for (int d = p.nr - 1; d >= 0; --d) {
+    if (!p2(p.r_ext[d])) return false;
+    for (int64_t t = 1; t < p.r_ext[d]; t <<= 1) ws.push_back(t * p.r_s[d]);
+  }
+  const int nb = (int)ws.size();
+  if (nb != lv + ln + lo || nb < 8) return false;
+  std::vector<int> nbit(nb, -1);                   // n-index bit, or -1 for a carry bit
+  std::vector<int64_t> xw(nb, 0);                  // X weight of a carry bit
+  for (int b = 0; b < nb; ++b) {
+    if (!p2(ws[b])) return false;
+    const int beta = lg(ws[b]);
+    if (beta < lv) xw[b] = vs << beta;
+    else if (beta < lv + ln) nbit[b] = beta - lv;
+    else xw[b] = ow[beta - lv - ln];
+  }
+  std::vector<char> in(nb, 0);
+  int td = 0;
+  auto ts_of = [&](int t) { return t - ln + lk; };
+  auto add = [&](int b) {
+    if (in[b] || td >= 12 || ts_of(td + 1) > 12 + (nbit[b] >= 0 ? 1 : 0)) return;
+    in[b] = 1;
+    ++td;
+  };
+  for (int b = 0; b < nb; ++b) if (nbit[b] >= 0) { in[b] = 1; ++td; }
+  if (ts_of(td) > 12 || td > 12) return false;
+  for (int b = 0; b < 3; ++b) add(b);
+  std::vector<int> bysrc;                          // carry bits by X weight
+  for (int b = 0; b < nb; ++b) if (nbit[b] < 0) bysrc.push_back(b);
+  std::stable_sort(bysrc.begin(), bysrc.end(), [&](int a, int b) { return xw[a] < xw[b]; });
+  for (int i = 0; i < 5 && i < (int)bysrc.size(); ++i) add(bysrc[i]);
+  for (int b = 3; b < 6 && b < nb; ++b) add(b);
+  for (int i = 5; i < (int)bysrc.size(); ++i) add(bysrc[i]);
+  for (int b = 0; b < 3; ++b) if (!in[b]) return false;
+  if (td > 12 || ts_of(td) > 12) return false;
+  const int cb = td - ln, tsb = cb + lk, TD = 1 << td;
+  std::vector<int> ebit;                           // carry tile bits in X-weight order
+  for (int b : bysrc) if (in[b]) ebit.push_back(b);
+  std::vector<int> epos(nb, -1);
+  for (int i = 0; i < cb; ++i) epos[ebit[i]] = i;
+  std::vector<int> fbit;
+  for (int b = 0; b < nb; ++b) if (in[b]) fbit.push_back(b);
+  tab.assign(128 + TD / 8 + (4096 + 256) / 4, 0);   // fc[4096] u16 then fn[256] u16
+  auto ew = [&](int i) { return i < cb ? xw[ebit[i]] : kw[i - cb]; };   // X weight of e bit i
+  for (int x = 0; x < 64; ++x)
+    for (int i = 0; i < 6; ++i) {
+      if ((x >> i & 1) && i < tsb) tab[x] += ew(i);
+      if ((x >> i & 1) && 6 + i < tsb) tab[64 + x] += ew(6 + i);
+    }
+  for (int q = 0; q < TD / 8; ++q)
+    for (int i = 3; i < td; ++i) if (q >> (i - 3) & 1) tab[128 + q] += int64_t(1) << fbit[i];
+  // f (dest-order tile index) is separable into its carry bits and its n bits
+  uint16_t* fc = reinterpret_cast<uint16_t*>(tab.data() + 128 + TD / 8);
+  uint16_t* fnn = fc + 4096;
+  std::vector<int32_t> cn(TD);
+  for (int f = 0; f < TD; ++f) {
+    int cp = 0, n = 0;
+    for (int i = 0; i < td; ++i)
+      if (f >> i & 1) {
+        if (nbit[fbit[i]] >= 0) n |= 1 << nbit[fbit[i]];
+        else cp |= 1 << epos[fbit[i]];
+      }
+    cn[f] = cp | (n << 16);
+    if (n == 0) fc[cp] = (uint16_t)f;
+    if (cp == 0) fnn[n] = (uint16_t)f;
+  }
+  for (int f = 0; f < TD; ++f)   // separability check: f = fc[carry] + fn[n]
+    if (fc[cn[f] & 0xFFFF] + fnn[cn[f] >> 16] != f) return false;
+  p.nc = 0;
+  for (int b = 0; b < nb; ++b)
+    if (!in[b]) {
+      if (p.nc >= TN_MAXD) return false;
+      p.c_src[p.nc] = xw[b];
+      p.c_dst[p.nc] = int64_t(1) << b;
+      ++p.nc;
+    }
+  p.nC = int64_t(1) << p.nc;
+  p.bp_t = td;
+  p.g_ts = tsb;
+  {                                                // 16-B pair loads: e bit 0 has X weight 1
+    bool vec = tsb >= 1 && ew(0) == 1;
+    for (int i = 1; i < tsb && vec; ++i) vec = ew(i) % 2 == 0;
+    for (int i = 0; i < p.nc && vec; ++i) vec = p.c_src[i] % 2 == 0;
+    p.bp_vec = vec ? 1 : 0;
+  }
+  p.g_cbits = cb;
+  p.g_N = (int32_t)e.N;
+  p.g_K = (int32_t)e.K;
+  p.T = TD;
+  p.g_nn = e.nn;
+  p.g_nk = e.nk;
+  for (int d = 0; d < e.nn; ++d) { p.gy_n_ext[d] = e.n_ext[d]; p.gy_n_s[d] = e.n_sb[d]; }
+  for (int d = 0; d < e.nk; ++d) { p.gy_k_ext[d] = e.k_ext[d]; p.gy_k_s[d] = e.k_sb[d]; }
+  // self-check (a few tiles): carry X offset and n index of every destination element
+  // against the plain decomposition of its S-output offset
+  auto xoff = [&](int64_t so) {                    // S-output offset -> (X offset of (o, v), n)
+    const int64_t v = so & (e.V - 1), o = so >> (lv + ln);
+    int64_t off = v * vs;
+    for (int i = 0; i < lo; ++i) if (o >> i & 1) off += ow[i];
+    return std::make_pair(off, (so >> lv) & (e.N - 1));
+  };
+  for (int64_t c : {int64_t(0), int64_t(1), p.nC / 3, p.nC - 1}) {
+    if (c < 0 || c >= p.nC) continue;
+    int64_t sc = 0, dc = 0;
+    for (int i = 0; i < p.nc; ++i) if ((c >> i) & 1) { sc += p.c_src[i]; dc += p.c_dst[i]; }
+    for (int f = 0; f < TD; ++f) {
+      const int cp = cn[f] & 0xFFFF, n = cn[f] >> 16;
+      const int64_t di = dc + tab[128 + (f >> 3)] + (f & 7);
+      int64_t so = 0;
+      for (int b = 0; b < nb; ++b) if (di >> b & 1) so += ws[b];
+      const auto ref = xoff(so);
+      if (sc + tab[cp & 63] + tab[64 + (cp >> 6)] != ref.first || n != ref.second) return false;
+      for (int k = 0; k < e.K; ++k) {         // the k part: kernel e index vs plain X offset
+        const int ek = cp + (k << cb);
+        int64_t kx = 0, t = k;
+        for (int d = e.nk - 1; d >= 0; --d) { kx += (t % e.k_ext[d]) * e.k_sa[d]; t /= e.k_ext[d]; }
+        if (ek >= (1 << tsb) || sc + tab[ek & 63] + tab[64 + (ek >> 6)] != ref.first + kx) return false;
+      }
+    }
+  }
+  return true;
+}
+
 // Operand-prep kernel choice: 1 = direct (source walks k with a
 // contiguous innermost k run of >= 8), 4 = bit-permutation transposer (power-of-
 // two extents), 2 = general transposer (blocks: the destination's contiguous
@@ -619,6 +781,10 @@ tn_status build_plan(tn_ctx* c) {
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
   const int dense_mode = env_int("TN_DENSE_MERGE", 1);     // 0 off, 1 cost rule, 2 always (tests)
+  // skinny steps folded into TC preps: correct (parity-tested) but the gate-prep kernel is
+  // still slower than skinny kernel + transposer on C4, so off by default
+  const int fold_gates = env_int("TN_FOLD_GATES", 0);
+  const int fold_maxk = env_int("TN_FOLD_MAXK", 64), fold_maxn = env_int("TN_FOLD_MAXN", 65535);
   const int wave_sync = env_int("TN_WAVE_SYNC", 1);        // GEMM wave synchronisation (L2 reuse)
                                                            // (2: column-contiguous case only)
   const int n_leaves = c->n_tensors;
@@ -688,6 +854,9 @@ tn_status build_plan(tn_ctx* c) {
   };
 
   Arena arena;
+  std::vector<std::vector<int64_t>> deferred(n_steps);   // arena releases moved to a later step
+  std::unordered_set<int> unalloc;                         // live ids = unmaterialised folded outputs
+  auto folded_out = [&](int id) { return unalloc.count(id) > 0; };
   std::vector<int32_t> tables;
   int64_t scratch = 0;
   c->steps.clear();
@@ -994,9 +1163,10 @@ tn_status build_plan(tn_ctx* c) {
       sp.g_blk_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.g_blk.begin(), sp.g_blk.end());
     }
+    const bool hinted = s < (int)c->fold_hint.size() && c->fold_hint[s] && consumer_step[s] > s;
     if (!sp.final_step) {
       sp.out_elems = out_elems;
-      sp.out_off = arena.alloc(out_elems);
+      sp.out_off = hinted ? 0 : arena.alloc(out_elems);   // folded: never materialised
       out.off = sp.out_off;
     }
     if (sp.tc) {
@@ -1019,9 +1189,18 @@ tn_status build_plan(tn_ctx* c) {
     } else {
       sp.einsum_idx = n_einsum++;
     }
-    // release consumed arena inputs (their only consumer is this step)
-    if (A.buf == 1) arena.release(A.off);
-    if (B.buf == 1) arena.release(B.off);
+    // release consumed arena inputs (their only consumer is this step); a folded step's
+    // inputs are read by its consumer's prep, so they are released there
+    if (hinted) {
+      if (A.buf == 1) deferred[consumer_step[s]].push_back(A.off);
+      if (B.buf == 1) deferred[consumer_step[s]].push_back(B.off);
+    } else {
+      if (A.buf == 1 && !(s > 0 && folded_out(sp.i))) arena.release(A.off);
+      if (B.buf == 1 && !(s > 0 && folded_out(sp.j))) arena.release(B.off);
+    }
+    for (int64_t off : deferred[s]) arena.release(off);
+    unalloc.erase(sp.j);
+    if (hinted) unalloc.insert(sp.i); else unalloc.erase(sp.i);
     live.erase(sp.j);
     live[sp.i] = out;
     sp.out = out;
@@ -1123,6 +1302,7 @@ tn_status build_plan(tn_ctx* c) {
   std::vector<std::pair<int, int64_t>> gt_ref;   // (prep index, offset in gt_all)
   std::vector<std::pair<int, int64_t>> rw_ref;   // grouped-merge row tables, same pool
   std::vector<std::pair<int, int64_t>> bp_ref;   // bit-permutation tile tables, same pool
+  std::vector<std::pair<int, int64_t>> gate_ref;  // gate-folded prep tables, same pool
   auto base_of = [&](const View& v) -> const float2* { return v.buf == 0 ? c->d_leaf : c->d_arena; };
   // rebuild the live views to fill descriptors (same replay as above)
   live.clear();
@@ -1254,6 +1434,8 @@ tn_status build_plan(tn_ctx* c) {
       e.acc = sp.final_step ? c->d_acc : nullptr;
       fill_shifts(e);
       sp.hdesc = e;
+      sp.x_slot = XV.absmax_slot;
+      sp.y_slot = YV.absmax_slot;
       if (c->debug_plan) {
         fprintf(stderr, "[tn] step %d simt mode %d M=%lld N=%lld K=%lld V=%lld vstride=%lld a_off%%2=%lld leaf=%d pow2=%d x:", s,
                 e.mode, (long long)e.M, (long long)e.N, (long long)e.K, (long long)e.V,
@@ -1550,6 +1732,60 @@ tn_status build_plan(tn_ctx* c) {
         }
       }
     }
+  // ---- gate folding: a skinny SIMT step (a small gate absorbed into a big tensor) whose
+  // output is a tensor-core operand is applied inside that operand's prep instead
+  const bool hint_pass = !c->fold_hint.empty();
+  if (fold_gates)
+    for (int s = 0; s < n_steps; ++s) {
+      StepPlan& cs = c->steps[s];
+      if (!cs.tc || cs.grouped || cs.dense_merge) continue;
+      for (int side = 0; side < 2; ++side) {
+        const int ps = side_producer[s][side];
+        if (ps < 0 || cs.skip_prep[side]) continue;
+        StepPlan& pp = c->steps[ps];
+        if (pp.tc || pp.mode != 1 || pp.final_step || pp.folded) continue;
+        if (pp.hdesc.K > fold_maxk || pp.hdesc.N > fold_maxn) continue;
+        if (hint_pass && !c->fold_hint[ps]) continue;
+        tn::PrepDesc& pd = pds[cs.prep_idx + side];
+        tn::PrepDesc trial = pd;
+        std::vector<int64_t> tab;
+        if (!plan_gate(trial, pp.hdesc, tab)) {
+          if (c->debug_plan) fprintf(stderr, "[tn] fold %d->%d side %d: no\n", ps, s, side);
+          continue;
+        }
+        if (c->debug_plan)
+          fprintf(stderr, "[tn] fold %d->%d side %d: yes (N=%lld K=%lld, tile 2^%d / src 2^%d)\n", ps, s, side,
+                  (long long)pp.hdesc.N, (long long)pp.hdesc.K, trial.bp_t, trial.g_ts);
+        trial.kind = 5;
+        trial.src = pp.hdesc.A;
+        trial.off = pp.hdesc.a_off;
+        trial.leaf = pp.hdesc.a_leaf;
+        trial.gy = pp.hdesc.B;
+        trial.gy_off = pp.hdesc.b_off;
+        trial.gy_leaf = pp.hdesc.b_leaf;
+        if (!c->host_only) {
+          trial.absmax_in = c->d_absmax + pp.x_slot;
+          trial.absmax_y = c->d_absmax + pp.y_slot;
+        }
+        pd = trial;
+        cs.r_fast[side] = 5;
+        cs.gtT[side] = trial.T;
+        gate_ref.push_back({cs.prep_idx + side, (int64_t)gt_all.size()});
+        gt_all.insert(gt_all.end(), tab.begin(), tab.end());
+        pp.folded = true;
+      }
+    }
+  {
+    std::vector<char> decided(n_steps, 0);
+    bool any = false;
+    for (int s = 0; s < n_steps; ++s) if (c->steps[s].folded) { decided[s] = 1; any = true; }
+    if (hint_pass) {
+      if (decided != c->fold_hint) return fail(TN_ERR_INTERNAL, "gate folding changed between planning passes");
+    } else if (any) {
+      c->fold_hint = decided;        // tn_set_slices re-plans with the folds' liveness
+      return TN_OK;
+    }
+  }
   if (c->host_only) {
     c->planned = true;
     return TN_OK;
@@ -1563,6 +1799,7 @@ tn_status build_plan(tn_ctx* c) {
     for (auto& r : gt_ref) pds[r.first].gt_tab = c->d_gt + r.second;
     for (auto& r : rw_ref) pds[r.first].rowoff = c->d_gt + r.second;
     for (auto& r : bp_ref) pds[r.first].bp_tab = c->d_gt + r.second;
+    for (auto& r : gate_ref) pds[r.first].bp_tab = c->d_gt + r.second;
   }
   if (n_prep) TN_CUDA(cudaMemcpyAsync(c->d_prep, pds.data(), n_prep * sizeof(tn::PrepDesc),
                                       cudaMemcpyHostToDevice, sm));
@@ -1607,6 +1844,7 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
   }
   for (size_t s = 0; s < c->steps.size(); ++s) {
     StepPlan& sp = c->steps[s];
+    if (!sp.tc && sp.folded) continue;      // applied inside its consumer's prep
     if (!sp.tc) {
       // first execution of an HBM-bound SIMT step: time every kernel variant on the
       // live operands (the step is idempotent unless it accumulates) and keep the
@@ -1996,8 +2234,12 @@ tn_status tn_set_slices(tn_ctx* c, int32_t n_sliced, const int64_t* sliced_label
     if (c->n_slices > INT64_MAX / c->dim_of[l]) return fail(TN_ERR_DATA, "too many slices");
     c->n_slices *= c->dim_of[l];
   }
+  // planning runs twice when gate folding applies: the first pass decides the folds,
+  // the second keeps the folded steps' inputs live until their consumers (fold_hint)
+  c->fold_hint.clear();
   tn_status st = build_plan(c);
-  if (st) { free_dev(c); return st; }
+  if (!st && !c->fold_hint.empty()) st = build_plan(c);
+  if (st) { free_dev(c); c->fold_hint.clear(); return st; }
   if (n_slices_out) *n_slices_out = c->n_slices;
   return TN_OK;
 }
@@ -2090,13 +2332,13 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"folded\":%s,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
              sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false",
              sp.tc ? (sp.skip_prep[0] ? -1 : sp.r_fast[0]) : -1,
              sp.tc ? (sp.skip_prep[1] ? -1 : sp.r_fast[1]) : -1, sp.planes_consumer >= 0 ? "true" : "false",
-             sp.dense_merge ? "true" : "false");
+             sp.dense_merge ? "true" : "false", sp.folded ? "true" : "false");
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";

@@ -68,6 +68,13 @@ struct PrepDesc {
   // [src lo/hi 128][dst T/8][slot T/4 words of u16][swizzle T/128 words of u8]
   int32_t bp_t, bp_vec;           // bp_vec: source pairs (e, e+1) are adjacent (16-B loads)
   const int64_t* bp_tab;
+  // gate-folded prep (kind 5): the operand is the output of a skinny SIMT step
+  // out[o][n][v] = sum_k Y[n][k] X[o, v, k] that is never materialised: src is X, the
+  // tile holds X values (carry bits + k bits), each plane element applies Y on the fly.
+  // bp_tab: [src lo/hi 128][dst T/8][cn: T int32 (carry pos | n << 16)]
+  const float2* gy; int64_t gy_off; int32_t gy_leaf, g_N, g_K, g_cbits, g_ts, g_nn, g_nk, pad_g;
+  int64_t gy_n_ext[8], gy_n_s[8], gy_k_ext[8], gy_k_s[8];
+  const unsigned* absmax_y;
   __half* dst; int64_t plane_elems;
   const unsigned* absmax_in;      // absmax of the source tensor (float bits)
   int* scale_out;                 // receives the exponent s (x * 2^s is split)

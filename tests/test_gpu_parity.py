@@ -150,6 +150,8 @@ ROUTES = {
                    "TN_FUSE_PLANES": "0"},
     "tc_dense_merge": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                        "TN_GROUP": "0", "TN_DENSE_MERGE": "2"},
+    "tc_folded": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8",
+                  "TN_SKINNY_MIN_BIG": "2", "TN_FOLD_GATES": "1"},
     "tc_grouped": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                    "TN_GROUP": "2"},
     "tc_pair": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
@@ -186,6 +188,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
         assert any(s["out_gen"] for s in steps)
         if mode != "single":     # a producer epilogue writes its consumer's fp16 planes
             assert any(s["planes_out"] for s in steps)
+    if route == "tc_folded":   # small gates applied inside tensor-core operand preps
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        assert any(s["folded"] for s in c.plan_json()["steps"])
     if route == "tc_dense_merge" and mode == "sparse":
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
