@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
 // 2 K absmax(X) absmax(Y) per real component (bound, no absmax of out exists).
 constexpr int GP_TMAX = 4096;
 constexpr int GP_KMAX = 16, GP_NMAX = 256;
-constexpr size_t GP_SMEM = GP_TMAX * 8 /*in*/ + GP_TMAX * 8 /*out*/ + 1024 * 8 /*Y*/ + 128 * 8 /*src*/ +
+constexpr size_t GP_SMEM = GP_TMAX * 8 /*in*/ + (GP_TMAX + GP_TMAX / 32) * 8 /*out, padded*/ + 1024 * 8 /*Y*/ + 128 * 8 /*src*/ +
                            GP_TMAX / 8 * 8 /*dst*/ + GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
 
 template <int PLANES>
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __res
   extern __shared__ __align__(16) uint8_t dyn[];
   float2* tin = reinterpret_cast<float2*>(dyn);                     // [TS] X values (carry, k)
   float2* tout = tin + GP_TMAX;                                      // [TD] outputs, dest order
-  float2* Ys = tout + GP_TMAX;                                       // [N][K]
+  float2* Ys = tout + GP_TMAX + GP_TMAX / 32;                        // [N][K]
   int64_t* s_src = reinterpret_cast<int64_t*>(Ys + 1024);            // [128]
   int64_t* s_dst = s_src + 128;                                      // [TD/8]
   uint16_t* s_fc = reinterpret_cast<uint16_t*>(s_dst + GP_TMAX / 8); // [2^cb] f of carry pos
@@ -560,14 +560,15 @@ __global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __res
             ai = fmaf(x[k].x, y.y, fmaf(x[k].y, y.x, ai));
           }
         }
-        tout[fcp + s_fn[n]] = make_float2(ar, ai);
+        const int f = fcp + s_fn[n];
+        tout[f + (f >> 5)] = make_float2(ar, ai);   // one pad slot per 32: strided writes spread
       }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
       float2 o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = tout[8 * q + j];
+      for (int j = 0; j < 8; ++j) o[j] = tout[8 * q + j + ((8 * q) >> 5)];
       split_store8<PLANES>(d, dc + s_dst[q], o, scale);
     }
   }

@@ -22,7 +22,7 @@ for mode in ["sparse", "single"]:
 '''
 base = {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8", "TN_SKINNY_MIN_BIG": "2",
         "ROOT": os.path.dirname(os.path.dirname(os.path.abspath(__file__)))}
-for extra in [{"TN_FOLD_GATES": "0"}, {}, {"TN_FOLD_MAXK": "1"}, {"TN_FOLD_MAXN": "1"}]:
+for extra in [{"TN_FOLD_GATES": "0"}, {"TN_FOLD_GATES": "1"}]:
     env = dict(os.environ, **base, **extra)
     r = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
     print(extra, r.stdout.strip(), r.stderr[-400:])
