@@ -113,7 +113,10 @@ TN_API tn_status tn_set_slices(tn_ctx* ctx, int32_t n_sliced, const int64_t* sli
  * path) and ADD each slice's root tensor into the context's fp64 accumulator
  * (fused slice-accumulate).  Repeating a range double-counts it.  Asynchronous.
  * precision / mixed_topk: see tn_precision.  TN_ERR_DATA if the range is not
- * inside [0, n_slices). */
+ * inside [0, n_slices).  The first slice a context executes runs every kernel
+ * launch directly (it tunes the SIMT kernel variants and seeds the delayed
+ * scaling of fused fp16 operand planes); later slices replay one captured CUDA
+ * graph of the per-slice launch sequence (not while profiling). */
 TN_API tn_status tn_contract(tn_ctx* ctx, int64_t slice_begin, int64_t slice_end,
                       tn_precision precision, int32_t mixed_topk);
 
@@ -123,7 +126,10 @@ TN_API tn_status tn_reset_accumulator(tn_ctx* ctx);
 /* Write the accumulated amplitudes, in the caller's sample order (full state:
  * index order), as complex128 (re, im) into the DEVICE buffer out[2*n_out].
  * n_out must equal n_samples (or 2^n_open for the full state; 1 when n_open = 0).
- * Asynchronous. */
+ * Synchronises once to read the fused-plane overflow flag: TN_ERR_DATA (and no
+ * output) if a producer epilogue's delayed-scaling margin was exceeded, i.e. the
+ * accumulated sum may contain saturated fp16 operands (rerun with
+ * TN_FUSE_PLANES=0); tn_reset_accumulator clears the flag. */
 TN_API tn_status tn_sum_slices(tn_ctx* ctx, double* out, int64_t n_out);
 
 /* Same as tn_sum_slices but into a HOST buffer; synchronises the stream. */
