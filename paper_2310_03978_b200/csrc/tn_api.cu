@@ -2196,7 +2196,15 @@ tn_status tn_upload_tensors(tn_ctx* c, const double* data) {
   if (!c || !c->loaded) return fail(TN_ERR_USAGE, "load a network first");
   if (c->host_only) return fail(TN_ERR_USAGE, "host-only context (device -1) cannot execute");
   if (!data) return fail(TN_ERR_USAGE, "data is NULL");
-  return upload_leaves(c, data);
+  tn_status st = upload_leaves(c, data);
+  if (st) return st;
+  if (c->planned && c->d_hist) {
+    // new tensor values: restart the delayed-scaling history; the next slice runs
+    // unfused and re-seeds it (SIMT variants and the captured graph are kept)
+    TN_CUDA(cudaMemsetAsync(c->d_hist, 0, c->steps.size() * sizeof(unsigned), c->stream));
+    c->tuned = false;
+  }
+  return TN_OK;
 }
 
 tn_status tn_set_path(tn_ctx* c, int32_t n_steps, const int32_t* pairs) {
