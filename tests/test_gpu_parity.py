@@ -412,3 +412,22 @@ def test_c2_sampled_slices_at_full_size(ctx):
         ref = oracle.contract_slice(w.net, w.path, fine, t, w.samples)
         assert rel_l2(got, ref) <= EXT_TOL
     c.close()
+
+
+def test_lxeb_of_gpu_amplitudes(ctx):
+    """The verification statistic of the paper (Eq. 2) on amplitudes the
+    library computes: 12-qubit circuit, full output state on the GPU, bitstrings drawn
+    from the oracle's |psi|^2 (exact sampling, F = 1) and uniformly (F = 0)."""
+    from paper_2310_03978_b200 import verify
+    w = configs.c1("full")
+    psi = oracle.statevector(w.circuit, gate_matrix)
+    amps, _ = run_gpu(ctx, w)
+    n = w.circuit.n_qubits
+    p = np.abs(psi) ** 2
+    rng = np.random.default_rng(13)
+    exact = rng.choice(p.size, size=20000, p=p / p.sum())
+    uniform = rng.integers(0, p.size, size=20000)
+    f_gpu, f_ref = verify.lxeb(amps[exact], n), verify.lxeb(psi[exact], n)
+    assert abs(f_gpu - f_ref) <= 1e-5 * abs(f_ref + 1.0)
+    assert abs(f_gpu - 1.0) < 5 * verify.lxeb_stderr(amps[exact], n)
+    assert abs(verify.lxeb(amps[uniform], n)) < 5 * verify.lxeb_stderr(amps[uniform], n)
