@@ -1027,6 +1027,78 @@ __global__ void __launch_bounds__(256) einsum_wide_old_kernel(const EinsumDesc* 
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// ---------------------------------------------------------------- SIMT einsum, warp dot
+// Batched merges with tiny per-batch outputs and a long K (e.g. the last merges of a
+// sparse-state path: J = 65 536 batches of 4 x 16 outputs, K = 2048): one warp per
+// output row (j, m) computes all N <= 32 outputs, lanes striding K (coalesced along
+// the operands' unit-stride k), fp32 lane sums reduced across the warp in fp64.
+constexpr int WD_NMAX = 32;
+__global__ void __launch_bounds__(256) einsum_wdot_kernel(const EinsumDesc* __restrict__ gd,
+                                                          const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  __shared__ int64_t boff[8][WD_NMAX];
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = (int)d.N;
+  const int64_t rows = d.J * d.M;
+  float amax = 0.f;
+  for (int64_t row = blockIdx.x * 8 + warp; row < rows; row += (int64_t)gridDim.x * 8) {
+    const int64_t m = row % d.M, j = row / d.M;
+    const int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs + decompose(m, d.nm, d.m_ext, d.m_sa);
+    if (lane < N)
+      boff[warp][lane] = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs + decompose(lane, d.nn, d.n_ext, d.n_sb);
+    __syncwarp();
+    float cr[WD_NMAX], ci[WD_NMAX];
+#pragma unroll
+    for (int n = 0; n < WD_NMAX; ++n) { cr[n] = 0.f; ci[n] = 0.f; }
+    for (int64_t k = lane; k < d.K; k += 32) {
+      int64_t ka = 0, kb = 0, t = k;
+      if (d.pow2) {                    // shift tables: no 64-bit division per k
+        for (int i = d.nk - 1; i >= 0; --i) {
+          const int sh = d.k_sh[i];
+          const int64_t dg = t & ((int64_t(1) << sh) - 1);
+          t >>= sh;
+          ka += dg * d.k_sa[i];
+          kb += dg * d.k_sb[i];
+        }
+      } else {
+        for (int i = d.nk - 1; i >= 0; --i) {
+          const int64_t dg = t % d.k_ext[i];
+          t /= d.k_ext[i];
+          ka += dg * d.k_sa[i];
+          kb += dg * d.k_sb[i];
+        }
+      }
+      const float2 a = __ldg(A + ao + ka);
+#pragma unroll
+      for (int n = 0; n < WD_NMAX; ++n) {
+        if (n < N) {
+          const float2 b = __ldg(B + boff[warp][n] + kb);
+          cr[n] = fmaf(a.x, b.x, fmaf(-a.y, b.y, cr[n]));
+          ci[n] = fmaf(a.x, b.y, fmaf(a.y, b.x, ci[n]));
+        }
+      }
+    }
+    double outr = 0.0, outi = 0.0;
+#pragma unroll
+    for (int n = 0; n < WD_NMAX; ++n) {
+      if (n < N) {
+        double r = cr[n], i = ci[n];
+        for (int o = 16; o > 0; o >>= 1) {
+          r += __shfl_xor_sync(0xffffffffu, r, o);
+          i += __shfl_xor_sync(0xffffffffu, i, o);
+        }
+        if (lane == n) { outr = r; outi = i; }
+      }
+    }
+    if (lane < N) store_out(d, row * N + lane, outr, outi, amax);
+    __syncwarp();
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
 // ---------------------------------------------------------------- SIMT einsum, split-K dot
 // Few outputs, long K (e.g. the last step of a closed network, a 2^30-long dot):
 // block b takes output p = b / nchunk and a kchunk range of k; fp64 block
@@ -1351,6 +1423,13 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     else if (h.K <= 4) launch_wide<4>(d_desc, h, leaf_off, smem, vec2, kpair, s);
     else if (h.K <= 8) launch_wide<8>(d_desc, h, leaf_off, smem, vec2, kpair, s);
     else launch_wide<16>(d_desc, h, leaf_off, smem, vec2, kpair, s);
+    return cudaGetLastError();
+  }
+  if (h.mode == 4) {
+    const int64_t rows = h.J * h.M;
+    int64_t blocks = (rows + 7) / 8;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    einsum_wdot_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(d_desc, leaf_off);
     return cudaGetLastError();
   }
   if (h.mode == 2) {

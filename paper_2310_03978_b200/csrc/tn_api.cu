@@ -772,6 +772,7 @@ tn_status build_plan(tn_ctx* c) {
   const int dot_min_k = env_int("TN_DOT_MIN_K", 4096);
   const int dot_max_out = env_int("TN_DOT_MAX_OUT", 4096);
   const int tc_deep_k = env_int("TN_TC_DEEP_K", 1024);
+  const int wdot_min_k = env_int("TN_WDOT_MIN_K", 256);    // SIMT mode 4 (warp dot) from this K
   const int skinny_max_small = env_int("TN_SKINNY_MAX_SMALL", 64);
   const int prep_force = env_int("TN_PREP_FORCE", -1);   // tests: force a prep kernel kind
   const int group_mode = env_int("TN_GROUP", 1);          // 0 off, 1 cost model, 2 always
@@ -1020,6 +1021,8 @@ tn_status build_plan(tn_ctx* c) {
       if (outs <= dot_max_out && sp.k >= dot_min_k) {
         sp.mode = 2;
         partial_elems = std::max(partial_elems, 2 * outs);
+      } else if (sp.merge && sp.J > 1 && sp.n <= 32 && sp.k >= wdot_min_k) {
+        sp.mode = 4;                  // batched merge, tiny outputs per batch, long K
       } else if (one_batch && skinny(sp.m, sp.n)) {
         sp.mode = 1;
         sp.x_is_b = false;
@@ -1468,6 +1471,7 @@ tn_status build_plan(tn_ctx* c) {
         e.partial = c->d_partial;
         e.kchunk = 1 << 16;
       }
+      if (sp.mode == 4) e.mode = 4;
       fill_shifts(e);
       sp.hdesc = e;
     } else {

@@ -27,7 +27,8 @@ struct EinsumDesc {
   int64_t k_ext[TN_MAXD], k_sa[TN_MAXD], k_sb[TN_MAXD];
   unsigned* absmax_out;           // nullable: atomicMax of |re|,|im| bits
   double2* acc;                   // nullable: acc[idx] += C instead of storing C
-  // mode: 0 general (one thread per output), 1 skinny (B = small operand staged in
+  // mode: 4 warp dot (batched merge, one warp per output row, N <= 32, lanes over K);
+  // 0 general (one thread per output), 1 skinny (B = small operand staged in
   // smem, output layout [Mo][N][V] with V = A's smallest-stride free dim, which is
   // m_ext/m_sa[nm-1] here), 2 split-K dot (few outputs, long K; fp64 partials)
   int32_t mode, pow2;             // pow2: every m/n/k extent is a power of two (shift tables valid)

@@ -130,6 +130,7 @@ ROUTES = {
     "simt_modes": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_DOT_MIN_K": "2",
                    "TN_DOT_MAX_OUT": "16"},
     "simt_wide": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SKINNY_MAX_SMALL": "0"},
+    "simt_wdot": {"TN_DISABLE_TC": "1", "TN_WDOT_MIN_K": "2"},
     "simt_variant1": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "1"},
     "simt_variant2": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "2"},
     "simt_variant3": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "3"},
@@ -188,6 +189,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
         assert any(s["out_gen"] for s in steps)
         if mode != "single":     # a producer epilogue writes its consumer's fp16 planes
             assert any(s["planes_out"] for s in steps)
+    if route == "simt_wdot" and mode == "sparse":
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        assert 4 in {s["mode"] for s in c.plan_json()["steps"]}
     if route == "tc_folded":   # small gates applied inside tensor-core operand preps
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
