@@ -633,13 +633,17 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
   const int K = (int)d.K, N = (int)d.N, Np = (N + 1) & ~1;
-  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [K][Np]
-  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * K * Np);
+  // batched merges (J > 1, R = 1): every slab of the small operand is staged, batch j
+  // reads X slab ia[j] and Y slab ib[j]; the output is [J][Xo][N][V]
+  const int GY = d.J > 1 ? (int)d.n_yslabs : 1;
+  float2* Bs = reinterpret_cast<float2*>(dyn);                 // [GY][K][Np]
+  int64_t* koff = reinterpret_cast<int64_t*>(dyn + sizeof(float2) * GY * K * Np);
   const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
   const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
-  for (int e = threadIdx.x; e < K * Np; e += blockDim.x) {
-    const int k = e / Np, n = e % Np;
-    Bs[e] = n < N ? B[decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)]
+  for (int e = threadIdx.x; e < GY * K * Np; e += blockDim.x) {
+    const int sy = e / (K * Np), ee = e % (K * Np);
+    const int k = ee / Np, n = ee % Np;
+    Bs[e] = n < N ? B[sy * d.b_gs + decompose(n, d.nn, d.n_ext, d.n_sb) + decompose(k, d.nk, d.k_ext, d.k_sb)]
                   : make_float2(0.f, 0.f);
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
@@ -647,7 +651,7 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
   // k values loaded per row before any use; R rows per thread (grid-stride apart, so
   // every warp access stays lane-coalesced): R·KU·VEC·8 B in flight per thread
   constexpr int KU = R == 4 ? 4 : (R == 2 ? (VEC == 2 ? 4 : 8) : (NMAX <= 16 ? 8 : 4));
-  const int64_t V = d.V, Vv = V / VEC, Mv = d.M / VEC;
+  const int64_t V = d.V, Vv = V / VEC, Mb = d.M / VEC, Mv = d.J * Mb;
   const int64_t vstride = d.m_sa[d.nm - 1];
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   float amax = 0.f;
@@ -655,15 +659,22 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
     const float2* a_row[R];
     int64_t obase[R];
     bool live[R];
+    int64_t bslab = 0;                 // J > 1 runs with R = 1
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int64_t m = m0 + r * step;
       live[r] = m < Mv;
-      const int64_t mm = live[r] ? m : m0;
+      int64_t mm = live[r] ? m : m0, jb = 0;
+      if (d.J > 1) {
+        jb = mm / Mb;
+        mm -= jb * Mb;
+      }
       const int64_t vi = (mm % Vv) * VEC, o = mm / Vv;
-      a_row[r] = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
-                           : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
-      obase[r] = o * N * V + vi;
+      a_row[r] = A + (d.J > 1 ? (int64_t)d.ia[jb] * d.a_gs : 0) +
+                 (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa) : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) +
+                 vi * vstride;
+      obase[r] = jb * d.M * N + o * N * V + vi;
+      if (r == 0 && d.J > 1) bslab = (int64_t)d.ib[jb] * K * Np;
     }
     float cr[R][VEC][NMAX], ci[R][VEC][NMAX];
 #pragma unroll
@@ -709,7 +720,7 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
 #pragma unroll
       for (int kk = 0; kk < KU; ++kk) {
         if (k0 + kk < K) {
-          const float4* brow = reinterpret_cast<const float4*>(Bs + (k0 + kk) * Np);
+          const float4* brow = reinterpret_cast<const float4*>(Bs + bslab + (k0 + kk) * Np);
 #pragma unroll
           for (int n2 = 0; n2 < NMAX / 2; ++n2) {
             if (2 * n2 < N) {
@@ -1307,7 +1318,7 @@ template <int NMAX, int VEC, int R>
 bool launch_skinny_r(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* leaf_off, size_t smem,
                      bool kpair, cudaStream_t s) {
   if constexpr (skinny_ok<NMAX, VEC, R>()) {
-    const int g = grid_for((h.M / VEC + R - 1) / R, 256);
+    const int g = grid_for((h.J * (h.M / VEC) + R - 1) / R, 256);
     if (VEC == 1 && kpair) einsum_skinny_kernel<NMAX, 1, true, 2, R><<<g, 256, smem, s>>>(d_desc, leaf_off);
     else einsum_skinny_kernel<NMAX, VEC, true, 1, R><<<g, 256, smem, s>>>(d_desc, leaf_off);
     return true;
@@ -1329,6 +1340,7 @@ void launch_skinny(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t*
     int R = (int)std::max<int64_t>(1, std::min<int64_t>(4, 16 / (kl * VEC)));
     if (rows) R = rows;
     if (rforce) R = rforce;
+    if (h.J > 1) R = 1;                // batched: one slab of the small operand per row
     if (R >= 4 && launch_skinny_r<NMAX, VEC, 4>(d_desc, h, leaf_off, smem, kpair, s)) return;
     if (R >= 2 && launch_skinny_r<NMAX, VEC, 2>(d_desc, h, leaf_off, smem, kpair, s)) return;
     launch_skinny_r<NMAX, VEC, 1>(d_desc, h, leaf_off, smem, kpair, s);
@@ -1344,7 +1356,8 @@ void launch_wide(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* l
 }
 
 int einsum_variants(const EinsumDesc& h) {
-  if (h.mode == 1) return 4;   // 0 heuristic rows, 1 previous design, 2..3: R = 1, 2 (new design)
+  if (h.mode == 1) return h.J > 1 ? 1 : 4;   // 0 heuristic rows, 1 previous design, 2..3: R = 1, 2
+                                             // (batched merges: the new design only)
   if (h.mode == 3) return 2;   // 0 new design, 1 previous design
   return 1;
 }
@@ -1368,7 +1381,7 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
   for (int i = 0; i < h.nm && kpair; ++i) kpair = h.m_sa[i] % 2 == 0 || h.m_ext[i] == 1;
   for (int i = 0; i + 1 < h.nk && kpair; ++i) kpair = h.k_sa[i] % 2 == 0;
   static const int simt_old = getenv("TN_SIMT_OLD") ? atoi(getenv("TN_SIMT_OLD")) : 0;
-  if ((simt_old || variant == 1) && (h.mode == 1 || h.mode == 3)) {
+  if ((simt_old || variant == 1) && (h.mode == 1 || h.mode == 3) && h.J == 1) {
     static bool attr = false;
     if (!attr) {
       allow_big_smem(einsum_skinny_old_kernel<4, true>); allow_big_smem(einsum_skinny_old_kernel<8, true>);
@@ -1405,7 +1418,8 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
   }
   if (h.mode == 1) {
     const int rows = variant >= 2 ? variant - 1 : 0;
-    const size_t smem = sizeof(float2) * h.K * ((h.N + 1) & ~1) + sizeof(int64_t) * h.K;
+    const size_t smem = sizeof(float2) * (h.J > 1 ? h.n_yslabs : 1) * h.K * ((h.N + 1) & ~1) +
+                        sizeof(int64_t) * h.K;
 #define TN_SKINNY(NM)                                                            \
   (vec2 && NM <= 16 ? launch_skinny<NM, 2>(d_desc, h, leaf_off, smem, false, rows, s)  \
                     : launch_skinny<NM, 1>(d_desc, h, leaf_off, smem, kpair, rows, s))

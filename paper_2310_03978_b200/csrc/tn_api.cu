@@ -1018,15 +1018,19 @@ tn_status build_plan(tn_ctx* c) {
         return big >= skinny_big && small <= skinny_max_small && small * sp.k <= 8192 && sp.k <= 256;
       };
       const bool one_batch = !sp.merge || sp.J == 1;   // J = 1 merges fold their slabs
+      // batched skinny (J > 1 merges): every slab of the small side staged in smem
+      auto batched_skinny = [&](int64_t big, int64_t small, int64_t gsmall) {
+        return sp.merge && sp.J > 1 && skinny(big, small) && gsmall * ((small + 1) & ~1) * sp.k <= 8192;
+      };
       if (outs <= dot_max_out && sp.k >= dot_min_k) {
         sp.mode = 2;
         partial_elems = std::max(partial_elems, 2 * outs);
       } else if (sp.merge && sp.J > 1 && sp.n <= 32 && sp.k >= wdot_min_k) {
         sp.mode = 4;                  // batched merge, tiny outputs per batch, long K
-      } else if (one_batch && skinny(sp.m, sp.n)) {
+      } else if ((one_batch && skinny(sp.m, sp.n)) || batched_skinny(sp.m, sp.n, gB.ext)) {
         sp.mode = 1;
         sp.x_is_b = false;
-      } else if (one_batch && skinny(sp.n, sp.m)) {
+      } else if ((one_batch && skinny(sp.n, sp.m)) || batched_skinny(sp.n, sp.m, gA.ext)) {
         sp.mode = 1;
         sp.x_is_b = true;
       } else if (one_batch) {
@@ -1046,7 +1050,8 @@ tn_status build_plan(tn_ctx* c) {
     std::vector<VDim> od;
     const auto& kc = consumer_k[s];
     if (sp.mode == 1 || sp.mode == 3) {
-      // output [X outer dims][Y dims][v], v = the big operand's smallest-stride dim
+      // output [J][X outer dims][Y dims][v], v = the big operand's smallest-stride dim
+      if (sp.merge && sp.J > 1) od.push_back({GROUP, sp.J, 0});
       const auto& X = sp.x_is_b ? FB : FA;
       std::vector<VDim> Y = sp.x_is_b ? FA : FB;
       // lane dims v: the contiguous run of X's memory that starts at its smallest
@@ -1413,7 +1418,7 @@ tn_status build_plan(tn_ctx* c) {
       e.mode = sp.mode;
       e.A = base_of(XV); e.B = base_of(YV); e.C = Cptr;
       e.a_off = XV.off; e.b_off = YV.off;
-      if (sp.merge) {   // J == 1: fold the single slab of each side into the offsets
+      if (sp.merge && sp.J == 1) {   // fold the single slab of each side into the offsets
         const int64_t sa = (int64_t)sp.ia[0] * gA.stride, sb = (int64_t)sp.ib[0] * gB.stride;
         e.a_off += sp.x_is_b ? sb : sa;
         e.b_off += sp.x_is_b ? sa : sb;
@@ -1421,6 +1426,16 @@ tn_status build_plan(tn_ctx* c) {
       e.a_leaf = XV.buf == 0 ? XV.leaf : -1;
       e.b_leaf = YV.buf == 0 ? YV.leaf : -1;
       e.J = 1;
+      if (sp.merge && sp.J > 1) {     // batched skinny: X / Y slabs per batch j
+        const int32_t* ta = c->host_only ? nullptr : c->d_tables + sp.ia_off;
+        const int32_t* tb = c->host_only ? nullptr : c->d_tables + sp.ib_off;
+        e.J = sp.J;
+        e.ia = sp.x_is_b ? tb : ta;
+        e.ib = sp.x_is_b ? ta : tb;
+        e.a_gs = sp.x_is_b ? gB.stride : gA.stride;
+        e.b_gs = sp.x_is_b ? gA.stride : gB.stride;
+        e.n_yslabs = sp.x_is_b ? gA.ext : gB.ext;
+      }
       e.M = sp.x_is_b ? sp.n : sp.m;
       e.N = sp.x_is_b ? sp.m : sp.n;
       e.K = sp.k;

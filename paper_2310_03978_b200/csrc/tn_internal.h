@@ -35,6 +35,7 @@ struct EinsumDesc {
   uint8_t m_sh[TN_MAXD], n_sh[TN_MAXD], k_sh[TN_MAXD];   // log2 of the extents
   int64_t V;                      // mode 1: extent of the vector (lane) dim
   double* partial;                // mode 2: fp64 partial sums [2*J*M*N] (zeroed per launch)
+  int64_t n_yslabs;               // mode 1 with J > 1: slabs of the small operand (all in smem)
   int64_t kchunk;                 // mode 2: k elements per block
 };
 
