@@ -1110,6 +1110,53 @@ __global__ void __launch_bounds__(256) einsum_wdot_kernel(const EinsumDesc* __re
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// Variant for operands whose unit stride is the output dim n: lane = (k group, n), so
+// each load instruction reads NL consecutive n of 32/NL k values; one fp32 partial per
+// lane, reduced across the k groups in fp64.
+__global__ void __launch_bounds__(256) einsum_wdot2_kernel(const EinsumDesc* __restrict__ gd,
+                                                           const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = (int)d.N;
+  int lnl = 0;
+  while ((1 << lnl) < N) ++lnl;
+  const int NL = 1 << lnl, G = 32 / NL;            // N <= 32: NL lanes per k group
+  const int n = lane & (NL - 1), kg = lane >> lnl;
+  const int64_t rows = d.J * d.M;
+  float amax = 0.f;
+  for (int64_t row = blockIdx.x * 8 + warp; row < rows; row += (int64_t)gridDim.x * 8) {
+    const int64_t m = row % d.M, j = row / d.M;
+    const int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs + decompose(m, d.nm, d.m_ext, d.m_sa);
+    const int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs + (n < N ? decompose(n, d.nn, d.n_ext, d.n_sb) : 0);
+    float cr = 0.f, ci = 0.f;
+    for (int64_t k = kg; k < d.K; k += G) {
+      int64_t ka = 0, kb = 0, t = k;
+      for (int i = d.nk - 1; i >= 0; --i) {
+        const int sh = d.k_sh[i];
+        const int64_t dg = d.pow2 ? (t & ((int64_t(1) << sh) - 1)) : t % d.k_ext[i];
+        t = d.pow2 ? (t >> sh) : t / d.k_ext[i];
+        ka += dg * d.k_sa[i];
+        kb += dg * d.k_sb[i];
+      }
+      if (n < N) {
+        const float2 a = __ldg(A + ao + ka), b = __ldg(B + bo + kb);
+        cr = fmaf(a.x, b.x, fmaf(-a.y, b.y, cr));
+        ci = fmaf(a.x, b.y, fmaf(a.y, b.x, ci));
+      }
+    }
+    double r = cr, i = ci;
+    for (int o = 16; o >= NL; o >>= 1) {
+      r += __shfl_xor_sync(0xffffffffu, r, o);
+      i += __shfl_xor_sync(0xffffffffu, i, o);
+    }
+    if (kg == 0 && n < N) store_out(d, row * N + n, r, i, amax);
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
 // ---------------------------------------------------------------- SIMT einsum, split-K dot
 // Few outputs, long K (e.g. the last step of a closed network, a 2^30-long dot):
 // block b takes output p = b / nchunk and a kchunk range of k; fp64 block
@@ -1359,6 +1406,7 @@ int einsum_variants(const EinsumDesc& h) {
   if (h.mode == 1) return h.J > 1 ? 1 : 4;   // 0 heuristic rows, 1 previous design, 2..3: R = 1, 2
                                              // (batched merges: the new design only)
   if (h.mode == 3) return 2;   // 0 new design, 1 previous design
+  if (h.mode == 4) return 2;   // 0 lanes over k, 1 lanes over (k group, n)
   return 1;
 }
 
@@ -1443,7 +1491,10 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     const int64_t rows = h.J * h.M;
     int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    einsum_wdot_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(d_desc, leaf_off);
+    if (variant == 1)
+      einsum_wdot2_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(d_desc, leaf_off);
+    else
+      einsum_wdot_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(d_desc, leaf_off);
     return cudaGetLastError();
   }
   if (h.mode == 2) {
