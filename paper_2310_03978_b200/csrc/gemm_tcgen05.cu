@@ -234,7 +234,11 @@ template <int PASSES, int EW, bool PAIR>
 __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<PASSES, PAIR>;
   constexpr int PLANES = C::PLANES, STAGES = C::STAGES;
-  constexpr uint32_t IDESC = Idesc<PAIR>::POS, IDESC_NEG = Idesc<PAIR>::NEG;
+  // narrow GEMMs (N <= 64): N = 64 MMAs (half the tensor work of the padded 128-wide
+  // tile); the pair's B halves become 32 rows each
+  const uint32_t IDESC = args.narrow ? ((Idesc<PAIR>::POS & ~(0x3Fu << 17)) | ((uint32_t)(64 >> 3) << 17))
+                                     : Idesc<PAIR>::POS;
+  const uint32_t IDESC_NEG = IDESC | (1u << 13);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
         const int sa = args.ia ? args.ia[j] : 0;
         const int sb = args.blk_slab_b ? args.blk_slab_b[mt] : (args.ib ? args.ib[j] : 0);
         const int arow = mt * C::TILE_M + (int)rank * BM;
-        const int brow = nt * BN + (int)rank * (BN / 2);
+        const int brow = nt * BN + (int)rank * (args.narrow ? 32 : BN / 2);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * C::STAGE_BYTES;
@@ -836,7 +840,10 @@ bool gemm_pair_ok(const GemmArgs& a, int min_m) {
   return min_m > 0 && a.M >= min_m && a.blk_slab_b == nullptr;
 }
 
-cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s) {
+cudaError_t launch_gemm(const GemmArgs& a_in, int passes, int num_sms, cudaStream_t s) {
+  GemmArgs a = a_in;
+  static const int narrow_on = getenv("TN_NARROW_MMA") ? atoi(getenv("TN_NARROW_MMA")) : 1;
+  a.narrow = (narrow_on && a.N <= 64) ? 1 : 0;
   if (a.wave_sync) {
     cudaError_t e = cudaMemsetAsync(a.wave_ctr, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;

@@ -134,7 +134,8 @@ struct GemmArgs {
   // dense merge (pair-mapped epilogue): row = a*2^pm_sh_m + p, col = b*2^pm_sh_n + q,
   // j = pair_map[a*pm_g1 + b] (-1: not a merged configuration), out C[j][p][q]
   const int32_t* pair_map;
-  int32_t pm_sh_m, pm_sh_n, pm_g1, pad_pm;
+  int32_t pm_sh_m, pm_sh_n, pm_g1;
+  int32_t narrow;                 // N <= 64: N = 64 MMA instructions (one column tile)
 };
 
 // ---------------------------------------------------------------- slice select

@@ -58,6 +58,8 @@ def crandn(rng, *shape):
     (5, 130, 70, 48, 3, 4),       # gather-batched (sparse einsum), tables
     (3, 600, 200, 64, 2, 3),      # batched, M > 512 (pair kernel by default), ragged
     (1, 256, 16, 8, 1, 1),        # narrow N, K < BK
+    (2, 700, 64, 96, 2, 2),       # narrow N = 64 (N = 64 MMAs, pair halves of 32 rows)
+    (1, 520, 40, 300, 1, 1),      # narrow, ragged N and K
 ])
 @pytest.mark.parametrize("passes", [3, 1])
 @pytest.mark.parametrize("pair", ["1", "0"])
