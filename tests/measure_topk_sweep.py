@@ -6,7 +6,7 @@ For k in {0, 1, 10, 50, all}: the k tensor-core steps with the largest T_cc run
   * time per C4 slice relative to all-1-pass (Table 3 column 3),
   * relative L2 and eps_L2^2 (Eq. 9) against the CPU oracle on a
     full-width C4 sample (sub-network with extra bonds fixed).
-    python tools/topk_sweep.py [out.json]
+    python tests/measure_topk_sweep.py [out.json]   (lives under tests/: it runs the oracle)
 """
 import json
 import os
