@@ -620,6 +620,19 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
             }
             continue;
           }
+          if (args.cols_stride > 1) {
+            // one strided column dim (the consumer's unit-stride dim is a row dim): a
+            // column's offset is n * stride, no table reads or contiguity tests
+            const int64_t cs = args.cols_stride;
+            float2* dst = args.C + rb + (int64_t)n0 * cs;
+#pragma unroll
+            for (int i = 0; i < WC; ++i) {
+              if (n0 + i >= args.N) continue;
+              dst[i * cs] = make_float2(sr[i], si[i]);
+              amax = fmaxf(amax, fmaxf(fabsf(sr[i]), fabsf(si[i])));
+            }
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < WC; i += 2) {      // full unroll: sr/si stay in registers
             if (n0 + i >= args.N) continue;

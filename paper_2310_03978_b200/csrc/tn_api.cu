@@ -787,6 +787,7 @@ tn_status build_plan(tn_ctx* c) {
   const int fold_gates = env_int("TN_FOLD_GATES", 0);
   const int fold_maxk = env_int("TN_FOLD_MAXK", 64), fold_maxn = env_int("TN_FOLD_MAXN", 65535);
   const int wave_sync = env_int("TN_WAVE_SYNC", 1);        // GEMM wave synchronisation (L2 reuse)
+  const int cols_single = env_int("TN_COLS_SINGLE", 1);    // strided single-dim column fast path
                                                            // (2: column-contiguous case only)
   const int n_leaves = c->n_tensors;
   const int n_steps = (int)c->path.size();
@@ -1632,6 +1633,14 @@ tn_status build_plan(tn_ctx* c) {
         for (int q = 0; q < g.n_po; ++q) { g.po_sh[q] = (uint8_t)lg(sp.po[q].ext); g.po_str[q] = sp.po[q].stride; }
         for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)lg(sp.qo[q].ext); g.qo_str[q] = sp.qo[q].stride; }
         g.cols_contig = (g.n_qo > 0 && g.qo_str[g.n_qo - 1] == 1 && g.qo_sh[g.n_qo - 1] >= 6) ? 1 : 0;
+        g.cols_stride = (cols_single && g.n_qo == 1 && g.qo_str[0] > 1) ? g.qo_str[0] : 0;
+        if (c->debug_plan) {
+          fprintf(stderr, "[tn] step %d out_gen M=%d N=%d rows:", s, g.M, g.N);
+          for (int q = 0; q < g.n_po; ++q) fprintf(stderr, " 2^%dx%lld", g.po_sh[q], (long long)g.po_str[q]);
+          fprintf(stderr, " | cols:");
+          for (int q = 0; q < g.n_qo; ++q) fprintf(stderr, " 2^%dx%lld", g.qo_sh[q], (long long)g.qo_str[q]);
+          fprintf(stderr, "\n");
+        }
       }
     }
     live.erase(sp.j);
@@ -1731,6 +1740,7 @@ tn_status build_plan(tn_ctx* c) {
         for (int q = 0; q < g.n_po; ++q) { g.po_sh[q] = (uint8_t)po[q].first; g.po_str[q] = po[q].second; }
         for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)qo[q].first; g.qo_str[q] = qo[q].second; }
         g.cols_contig = 0;   // plane mode has its own 8-column vectors
+        g.cols_stride = 0;
         int lk = 0;
         while ((int64_t(1) << lk) < pp.k) ++lk;
         g.plane_exp = -16 - lk;

@@ -110,6 +110,8 @@ struct GemmArgs {
   // ([P keep][Q keep][contracted, sorted]) so the consumer's operand is K-contiguous.
   int32_t out_gen, n_po, n_qo;
   int32_t cols_contig;            // out_gen: the 64 columns of a warp are one contiguous run
+  int32_t cols_pad;
+  int64_t cols_stride;            // out_gen: > 1 = the columns are one dim of this stride
   uint8_t po_sh[16], qo_sh[16];
   int64_t po_str[16], qo_str[16];
   // fused consumer prep (a3 + a6 in this epilogue): the output is written directly as the
