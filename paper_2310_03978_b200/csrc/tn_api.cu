@@ -787,6 +787,7 @@ tn_status build_plan(tn_ctx* c) {
   const int fold_gates = env_int("TN_FOLD_GATES", 0);
   const int fold_maxk = env_int("TN_FOLD_MAXK", 64), fold_maxn = env_int("TN_FOLD_MAXN", 65535);
   const int wave_sync = env_int("TN_WAVE_SYNC", 1);        // GEMM wave synchronisation (L2 reuse)
+  const int wave_min_k = env_int("TN_WAVE_MIN_K", 1024);   // ... for GEMMs with K >= this
   const int cols_single = env_int("TN_COLS_SINGLE", 1);    // strided single-dim column fast path
                                                            // (2: column-contiguous case only)
   const int n_leaves = c->n_tensors;
@@ -1624,7 +1625,7 @@ tn_status build_plan(tn_ctx* c) {
       }
       g.use_pair = tn::gemm_pair_ok(g, pair_min_m) ? 1 : 0;
       g.wave_ctr = c->d_wave;
-      g.wave_sync = (wave_sync && sp.k >= 1024) ? 1 : 0;
+      g.wave_sync = (wave_sync && sp.k >= wave_min_k) ? 1 : 0;
       g.out_gen = sp.out_gen ? 1 : 0;
       if (sp.out_gen) {
         auto lg = [](int64_t x) { int q = 0; while ((int64_t(1) << q) < x) ++q; return q; };
