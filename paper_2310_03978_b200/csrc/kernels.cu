@@ -466,24 +466,26 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
 // written.  Saves the skinny step's full pass over the big tensor.  Scale: |out| <=
 // 2 K absmax(X) absmax(Y) per real component (bound, no absmax of out exists).
 constexpr int GP_TMAX = 4096;
-constexpr int GP_KMAX = 16, GP_NMAX = 256;
-constexpr size_t GP_SMEM = GP_TMAX * 8 /*in*/ + (GP_TMAX + GP_TMAX / 32) * 8 /*out, padded*/ + 1024 * 8 /*Y*/ + 128 * 8 /*src*/ +
-                           GP_TMAX / 8 * 8 /*dst*/ + GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
+constexpr int GP_YMAX = 512, GP_NMAX = 256;
+constexpr int GP_BUF = GP_TMAX + GP_TMAX / 32;     // X tile, then (aliased) the padded output tile
+constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX / 8 * 8 /*dst*/ +
+                           GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
 
-template <int PLANES>
-__global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __restrict__ gd,
+// KT = K (gate inputs per output); a thread owns 16/KT carry positions, whose 16 X values
+// it keeps in registers, so the X tile's smem is reused for the outputs (4 blocks/SM)
+template <int PLANES, int KT>
+__global__ void __launch_bounds__(256, 3) prep_gate_kernel(const PrepDesc* __restrict__ gd,
                                                            const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) PrepDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
-  float2* tin = reinterpret_cast<float2*>(dyn);                     // [TS] X values (carry, k)
-  float2* tout = tin + GP_TMAX;                                      // [TD] outputs, dest order
-  float2* Ys = tout + GP_TMAX + GP_TMAX / 32;                        // [N][K]
-  int64_t* s_src = reinterpret_cast<int64_t*>(Ys + 1024);            // [128]
-  int64_t* s_dst = s_src + 128;                                      // [TD/8]
-  uint16_t* s_fc = reinterpret_cast<uint16_t*>(s_dst + GP_TMAX / 8); // [2^cb] f of carry pos
-  uint16_t* s_fn = s_fc + GP_TMAX;                                   // [N] f of n index
-  const int TD = 1 << d.bp_t, TS = 1 << d.g_ts, K = d.g_K, N = d.g_N, CB = 1 << d.g_cbits;
+  float2* buf = reinterpret_cast<float2*>(dyn);                      // [GP_BUF]
+  float2* Ys = buf + GP_BUF;                                          // [N][KT]
+  int64_t* s_src = reinterpret_cast<int64_t*>(Ys + GP_YMAX);          // [128]
+  int64_t* s_dst = s_src + 128;                                       // [TD/8]
+  uint16_t* s_fc = reinterpret_cast<uint16_t*>(s_dst + GP_TMAX / 8);  // [2^cb]
+  uint16_t* s_fn = s_fc + GP_TMAX;                                    // [N]
+  const int TD = 1 << d.bp_t, TS = 1 << d.g_ts, N = d.g_N, CB = 1 << d.g_cbits;
   {
     const int64_t* tab = d.bp_tab;
     for (int i = threadIdx.x; i < 128; i += blockDim.x) s_src[i] = tab[i];
@@ -492,15 +494,15 @@ __global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __res
     for (int i = threadIdx.x; i < CB; i += blockDim.x) s_fc[i] = fc[i];
     for (int i = threadIdx.x; i < N; i += blockDim.x) s_fn[i] = fc[GP_TMAX + i];
     const float2* Y = d.gy + d.gy_off + (d.gy_leaf >= 0 ? leaf_off[d.gy_leaf] : 0);
-    for (int e = threadIdx.x; e < N * K; e += blockDim.x) {
-      const int n = e / K, k = e % K;
+    for (int e = threadIdx.x; e < N * KT; e += blockDim.x) {
+      const int n = e / KT, k = e % KT;
       Ys[e] = Y[decompose(n, d.g_nn, d.gy_n_ext, d.gy_n_s) + decompose(k, d.g_nk, d.gy_k_ext, d.gy_k_s)];
     }
   }
   const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
   float scale;
   {
-    const float bound = 2.f * (float)K * __uint_as_float(*d.absmax_in) * __uint_as_float(*d.absmax_y);
+    const float bound = 2.f * (float)KT * __uint_as_float(*d.absmax_in) * __uint_as_float(*d.absmax_y);
     int s = 0;
     if (bound > 0.f) {
       int e;
@@ -511,13 +513,14 @@ __global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __res
     scale = ldexpf(1.0f, s);
   }
   const bool vec = d.bp_vec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  constexpr int CPT = 16 / KT;                    // carry positions per thread
   for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
     int64_t sc = 0, dc = 0;
     for (int i = 0; i < d.nc; ++i)
       if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
-    __syncthreads();   // tables / Y ready, previous tile consumed
+    __syncthreads();   // tables / Y ready, previous tile's outputs consumed
     const float2* sp = src + sc;
-    if (vec) {           // e, e+1 adjacent in X: 16-B loads
+    if (vec) {
       float4 v[GP_TMAX / 512];
 #pragma unroll
       for (int i = 0; i < GP_TMAX / 512; ++i) {
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __res
 #pragma unroll
       for (int i = 0; i < GP_TMAX / 512; ++i) {
         const int e = 2 * (threadIdx.x + i * 256);
-        if (e < TS) *reinterpret_cast<float4*>(tin + e) = v[i];
+        if (e < TS) *reinterpret_cast<float4*>(buf + e) = v[i];
       }
     } else {
       float2 v[GP_TMAX / 256];
@@ -539,36 +542,41 @@ __global__ void __launch_bounds__(256, 2) prep_gate_kernel(const PrepDesc* __res
 #pragma unroll
       for (int i = 0; i < GP_TMAX / 256; ++i) {
         const int e = threadIdx.x + i * 256;
-        if (e < TS) tin[e] = v[i];
+        if (e < TS) buf[e] = v[i];
       }
     }
     __syncthreads();
-    // one thread per carry position: its K X values in registers, all N outputs
-    for (int cp = threadIdx.x; cp < CB; cp += blockDim.x) {
-      float2 x[GP_KMAX];
+    float2 xs[CPT][KT];
 #pragma unroll
-      for (int k = 0; k < GP_KMAX; ++k) x[k] = k < K ? tin[cp + k * CB] : make_float2(0.f, 0.f);
+    for (int i = 0; i < CPT; ++i) {
+      const int cp = threadIdx.x + i * 256;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) xs[i][k] = cp < CB ? buf[cp + k * CB] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();   // X tile read into registers: buf becomes the output tile
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int cp = threadIdx.x + i * 256;
+      if (cp >= CB) continue;
       const int fcp = s_fc[cp];
       for (int n = 0; n < N; ++n) {
-        const float2* yr = Ys + n * K;
+        const float2* yr = Ys + n * KT;
         float ar = 0.f, ai = 0.f;
 #pragma unroll
-        for (int k = 0; k < GP_KMAX; ++k) {
-          if (k < K) {
-            const float2 y = yr[k];
-            ar = fmaf(x[k].x, y.x, fmaf(-x[k].y, y.y, ar));
-            ai = fmaf(x[k].x, y.y, fmaf(x[k].y, y.x, ai));
-          }
+        for (int k = 0; k < KT; ++k) {
+          const float2 y = yr[k];
+          ar = fmaf(xs[i][k].x, y.x, fmaf(-xs[i][k].y, y.y, ar));
+          ai = fmaf(xs[i][k].x, y.y, fmaf(xs[i][k].y, y.x, ai));
         }
         const int f = fcp + s_fn[n];
-        tout[f + (f >> 5)] = make_float2(ar, ai);   // one pad slot per 32: strided writes spread
+        buf[f + (f >> 5)] = make_float2(ar, ai);
       }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
       float2 o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = tout[8 * q + j + ((8 * q) >> 5)];
+      for (int j = 0; j < 8; ++j) o[j] = buf[8 * q + j + ((8 * q) >> 5)];
       split_store8<PLANES>(d, dc + s_dst[q], o, scale);
     }
   }
@@ -1240,23 +1248,41 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int PLANES, int KT>
+cudaError_t launch_gate_t(const PrepDesc* d_desc, int g, const int64_t* leaf_off, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prep_gate_kernel<PLANES, KT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prep_gate_kernel<PLANES, KT><<<g, 256, GP_SMEM, s>>>(d_desc, leaf_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate(const PrepDesc* d_desc, int planes, int k, int g, const int64_t* leaf_off,
+                        cudaStream_t s) {
+#define TN_GATE(P)                                                        \
+  switch (k) {                                                            \
+    case 1: return launch_gate_t<P, 1>(d_desc, g, leaf_off, s);           \
+    case 2: return launch_gate_t<P, 2>(d_desc, g, leaf_off, s);           \
+    case 4: return launch_gate_t<P, 4>(d_desc, g, leaf_off, s);           \
+    case 8: return launch_gate_t<P, 8>(d_desc, g, leaf_off, s);           \
+    case 16: return launch_gate_t<P, 16>(d_desc, g, leaf_off, s);         \
+    default: return cudaErrorInvalidValue;                                \
+  }
+  if (planes == 4) { TN_GATE(4) } else { TN_GATE(2) }
+#undef TN_GATE
+}
+
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
-                        const int64_t* leaf_off, cudaStream_t s) {
+                        const int64_t* leaf_off, cudaStream_t s, int gate_k) {
   const int th = 256;
-  if (kind == 5) {   // gate-folded prep
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(prep_gate_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
-      cudaFuncSetAttribute(prep_gate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
-      attr = true;
-    }
+  if (kind == 5) {   // gate-folded prep (K = 1, 2, 4, 8 or 16, carried in the descriptor)
     const int64_t tiles = total / std::max(tile_T, 1);
-    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 2);
-    if (planes == 4)
-      prep_gate_kernel<4><<<g, th, GP_SMEM, s>>>(d_desc, leaf_off);
-    else
-      prep_gate_kernel<2><<<g, th, GP_SMEM, s>>>(d_desc, leaf_off);
-    return cudaGetLastError();
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 3);
+    return launch_gate(d_desc, planes, gate_k, g, leaf_off, s);
   }
   if (kind == 4) {   // bit-permutation transposer, tiles of tile_T <= 4096 elements
     static bool attr = false;

@@ -109,6 +109,7 @@ struct StepPlan {
   // reads fp16 planes its producer's epilogue wrote (no prep launch); planes_consumer =
   // the step whose planes this step's epilogue writes (-1: writes complex64)
   bool skip_prep[2] = {false, false};
+  int gate_k[2] = {0, 0};       // gate-folded prep: K of the folded gate per side
   int planes_consumer = -1;
   tn::GemmArgs gemm_plain;      // the step's GEMM without fusion (first, absmax-seeding slice)
 };
@@ -439,7 +440,7 @@ bool plan_gate(tn::PrepDesc& p, const tn::EinsumDesc& e, std::vector<int64_t>& t
   auto lg = [](int64_t x) { int q = 0; while ((int64_t(1) << q) < x) ++q; return q; };
   if (p.Kpad != p.K || p.K < 8 || !p2(p.K) || !p2(p.R) || p.G != 1 || p.rowoff) return false;
   if (e.mode != 1 || e.J != 1 || e.acc || !p2(e.N) || !p2(e.K) || !p2(e.V) || !p2(e.M)) return false;
-  if (e.N * e.K > 1024 || e.N > 256 || e.K > 16 || e.nn > 8 || e.nk > 8) return false;
+  if (e.N * e.K > 512 || e.N > 256 || e.K > 16 || e.nn > 8 || e.nk > 8) return false;
   const int lv = lg(e.V), ln = lg(e.N), lk = lg(e.K), lo = lg(e.M / e.V);
   // X weight of each o-index bit (Xo dims, outer -> inner in m_ext / m_sa [0, nm-1))
   std::vector<int64_t> ow;
@@ -782,10 +783,10 @@ tn_status build_plan(tn_ctx* c) {
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
   const int dense_mode = env_int("TN_DENSE_MERGE", 1);     // 0 off, 1 cost rule, 2 always (tests)
-  // skinny steps folded into TC preps: correct (parity-tested) but the gate-prep kernel is
-  // still slower than skinny kernel + transposer on C4, so off by default
-  const int fold_gates = env_int("TN_FOLD_GATES", 0);
-  const int fold_maxk = env_int("TN_FOLD_MAXK", 64), fold_maxn = env_int("TN_FOLD_MAXN", 65535);
+  // skinny steps folded into TC preps; gates with K > 8 stay separate
+  // (their gate-prep is slower than skinny kernel + transposer on C4)
+  const int fold_gates = env_int("TN_FOLD_GATES", 1);
+  const int fold_maxk = env_int("TN_FOLD_MAXK", 8), fold_maxn = env_int("TN_FOLD_MAXN", 65535);
   const int wave_sync = env_int("TN_WAVE_SYNC", 1);        // GEMM wave synchronisation (L2 reuse)
   const int wave_min_k = env_int("TN_WAVE_MIN_K", 1024);   // ... for GEMMs with K >= this
   const int cols_single = env_int("TN_COLS_SINGLE", 1);    // strided single-dim column fast path
@@ -1800,6 +1801,7 @@ tn_status build_plan(tn_ctx* c) {
         pd = trial;
         cs.r_fast[side] = 5;
         cs.gtT[side] = trial.T;
+        cs.gate_k[side] = (int)pp.hdesc.K;
         gate_ref.push_back({cs.prep_idx + side, (int64_t)gt_all.size()});
         gt_all.insert(gt_all.end(), tab.begin(), tab.end());
         pp.folded = true;
@@ -1910,7 +1912,7 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
         if (fused && sp.skip_prep[side]) continue;   // planes written by the producer's epilogue
         Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes), (int)s, sm);
         TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
-                                sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm));
+                                sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm, sp.gate_k[side]));
       }
       tn::GemmArgs ga = fused ? sp.gemm : sp.gemm_plain;
       ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;

@@ -160,7 +160,7 @@ struct SliceDesc {
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
 cudaError_t launch_set_counter(int64_t* counter, int64_t value, cudaStream_t s);
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
-                        const int64_t* leaf_off, cudaStream_t s);
+                        const int64_t* leaf_off, cudaStream_t s, int gate_k = 0);
 // variant: kernel variant of the SIMT mode (0 = heuristic); einsum_variants() = how many
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
                           const int64_t* leaf_off, cudaStream_t s, int variant = 0);

@@ -155,7 +155,9 @@ ROUTES = {
     "tc_dense_merge": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                        "TN_GROUP": "0", "TN_DENSE_MERGE": "2"},
     "tc_folded": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8",
-                  "TN_SKINNY_MIN_BIG": "2", "TN_FOLD_GATES": "1"},
+                  "TN_SKINNY_MIN_BIG": "2", "TN_FOLD_GATES": "1", "TN_FOLD_MAXK": "16"},
+    "tc_unfolded": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "8",
+                    "TN_SKINNY_MIN_BIG": "2", "TN_FOLD_GATES": "0"},
     "tc_grouped": {"TN_TC_MIN_BIG": "2", "TN_TC_MIN_SMALL": "1", "TN_TC_MIN_K": "2",
                    "TN_GROUP": "2"},
     "tc_pair": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
