@@ -336,12 +336,20 @@ def test_c4_bench_workload_sampled_subslice(ctx):
     c.contract(0, 1)
     got = c.sum_slices_host()
     info = c.info()
+    # the same slice again: now with fused fp16 operand planes (delayed scaling seeded
+    # by the first pass) and replayed as a CUDA graph
+    c.reset_accumulator()
+    c.contract(0, 1)
+    got2 = c.sum_slices_host()
+    steps = c.plan_json()["steps"]
     c.close()
     ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
-    err = rel_l2(got, ref)
+    err, err2 = rel_l2(got, ref), rel_l2(got2, ref)
     print(f"C4 sub-slice: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
-          f"tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}")
+          f"tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}; fused pass {err2:.3e} "
+          f"({sum(s['planes_out'] for s in steps)} plane producers, {sum(s['folded'] for s in steps)} folded gates)")
     assert err <= EXT_TOL
+    assert err2 <= EXT_TOL
 
 
 @pytest.mark.timeout(900)
