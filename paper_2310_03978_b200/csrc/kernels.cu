@@ -520,29 +520,35 @@ __global__ void __launch_bounds__(256, 3) prep_gate_kernel(const PrepDesc* __res
       if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
     __syncthreads();   // tables / Y ready, previous tile's outputs consumed
     const float2* sp = src + sc;
-    if (vec) {
-      float4 v[GP_TMAX / 512];
+    if (vec) {           // two rounds of 4 x 16-B loads in flight (keeps registers for xs)
 #pragma unroll
-      for (int i = 0; i < GP_TMAX / 512; ++i) {
-        const int e = 2 * (threadIdx.x + i * 256);
-        if (e < TS) v[i] = __ldg(reinterpret_cast<const float4*>(sp + s_src[e & 63] + s_src[64 + (e >> 6)]));
-      }
+      for (int h = 0; h < 2; ++h) {
+        float4 v[GP_TMAX / 1024];
 #pragma unroll
-      for (int i = 0; i < GP_TMAX / 512; ++i) {
-        const int e = 2 * (threadIdx.x + i * 256);
-        if (e < TS) *reinterpret_cast<float4*>(buf + e) = v[i];
+        for (int i = 0; i < GP_TMAX / 1024; ++i) {
+          const int e = 2 * (threadIdx.x + (h * GP_TMAX / 1024 + i) * 256);
+          if (e < TS) v[i] = __ldg(reinterpret_cast<const float4*>(sp + s_src[e & 63] + s_src[64 + (e >> 6)]));
+        }
+#pragma unroll
+        for (int i = 0; i < GP_TMAX / 1024; ++i) {
+          const int e = 2 * (threadIdx.x + (h * GP_TMAX / 1024 + i) * 256);
+          if (e < TS) *reinterpret_cast<float4*>(buf + e) = v[i];
+        }
       }
     } else {
-      float2 v[GP_TMAX / 256];
 #pragma unroll
-      for (int i = 0; i < GP_TMAX / 256; ++i) {
-        const int e = threadIdx.x + i * 256;
-        if (e < TS) v[i] = __ldg(sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
-      }
+      for (int h = 0; h < 2; ++h) {
+        float2 v[GP_TMAX / 512];
 #pragma unroll
-      for (int i = 0; i < GP_TMAX / 256; ++i) {
-        const int e = threadIdx.x + i * 256;
-        if (e < TS) buf[e] = v[i];
+        for (int i = 0; i < GP_TMAX / 512; ++i) {
+          const int e = threadIdx.x + (h * GP_TMAX / 512 + i) * 256;
+          if (e < TS) v[i] = __ldg(sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+        }
+#pragma unroll
+        for (int i = 0; i < GP_TMAX / 512; ++i) {
+          const int e = threadIdx.x + (h * GP_TMAX / 512 + i) * 256;
+          if (e < TS) buf[e] = v[i];
+        }
       }
     }
     __syncthreads();
