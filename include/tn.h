@@ -92,7 +92,10 @@ TN_API tn_status tn_load_network(tn_ctx* ctx, int32_t n_tensors, const int32_t* 
                           int64_t n_samples, const uint8_t* samples);
 
 /* Replace the tensor values of the loaded network (same layout as `data` above,
- * host pointer) without re-planning: host->device copy on the context stream. */
+ * host pointer) without re-planning: host->device copy on the context stream.  If any
+ * leaf's max |Re|,|Im| grows, the fp16-plane delayed-scaling history restarts and the
+ * next slice runs unfused; otherwise the history and the captured CUDA
+ * graph are kept. */
 TN_API tn_status tn_upload_tensors(tn_ctx* ctx, const double* data);
 
 /* Set the contraction path (§3.1): n_steps = N-1 pairs (i, j) of tensor

@@ -202,6 +202,7 @@ struct tn_ctx {
   unsigned* d_hist = nullptr;      // delayed scaling: running output absmax per step
   int* d_pexp = nullptr;           // delayed scaling: exponent per step (slice_select)
   int* d_flag = nullptr;           // fused plane overflow flag
+  double2* d_gather = nullptr;     // tn_sum_slices_host staging (n_out amplitudes)
   unsigned long long* d_wave = nullptr;   // GEMM wave-sync counter
   int64_t* d_gt = nullptr;         // general-transposer tile tables
   int64_t device_bytes = 0;
@@ -245,7 +246,7 @@ void free_dev(tn_ctx* c) {
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
                   c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt,
-                  c->d_hist, c->d_pexp, c->d_flag, c->d_wave};
+                  c->d_hist, c->d_pexp, c->d_flag, c->d_wave, c->d_gather};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
@@ -255,6 +256,7 @@ void free_dev(tn_ctx* c) {
   c->d_partial = nullptr;
   c->d_gt = nullptr;
   c->d_hist = nullptr; c->d_pexp = nullptr; c->d_flag = nullptr; c->d_wave = nullptr;
+  c->d_gather = nullptr;
   c->planned = false;
 }
 
@@ -1264,6 +1266,7 @@ tn_status build_plan(tn_ctx* c) {
   if ((st = dev_alloc(c, &c->d_pexp, (size_t)n_steps))) return st;
   if ((st = dev_alloc(c, &c->d_flag, 1))) return st;
   if ((st = dev_alloc(c, &c->d_wave, 1))) return st;
+  if ((st = dev_alloc(c, &c->d_gather, (size_t)std::max<int64_t>(c->n_out, 1)))) return st;
   TN_CUDA(cudaMemsetAsync(c->d_hist, 0, n_steps * sizeof(unsigned), sm));
   TN_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), sm));
   if (!tables.empty())
@@ -2228,11 +2231,16 @@ tn_status tn_upload_tensors(tn_ctx* c, const double* data) {
   if (!c || !c->loaded) return fail(TN_ERR_USAGE, "load a network first");
   if (c->host_only) return fail(TN_ERR_USAGE, "host-only context (device -1) cannot execute");
   if (!data) return fail(TN_ERR_USAGE, "data is NULL");
+  const std::vector<float> before = c->leaf_absmax;
   tn_status st = upload_leaves(c, data);
   if (st) return st;
-  if (c->planned && c->d_hist) {
-    // new tensor values: restart the delayed-scaling history; the next slice runs
-    // unfused and re-seeds it (SIMT variants and the captured graph are kept)
+  bool grew = before.size() != c->leaf_absmax.size();
+  for (size_t t = 0; t < before.size() && !grew; ++t) grew = c->leaf_absmax[t] > before[t];
+  if (c->planned && c->d_hist && grew) {
+    // a leaf got larger: restart the delayed-scaling history; the next slice runs
+    // unfused and re-seeds it (SIMT variants and the captured graph are kept).  Values
+    // no larger than before keep the history (the 32x margin and the overflow check
+    // cover the slice-to-slice variation).
     TN_CUDA(cudaMemsetAsync(c->d_hist, 0, c->steps.size() * sizeof(unsigned), c->stream));
     c->tuned = false;
   }
@@ -2330,11 +2338,9 @@ tn_status tn_sum_slices_host(tn_ctx* c, double* out_host, int64_t n_out) {
   if (st) return st;
   if ((st = check_plane_overflow(c))) return st;
   if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
-  double2* tmp = nullptr;
-  TN_CUDA(cudaMallocAsync(&tmp, n_out * sizeof(double2), c->stream));
-  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, tmp, n_out, c->stream));
-  TN_CUDA(cudaMemcpyAsync(out_host, tmp, n_out * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
-  TN_CUDA(cudaFreeAsync(tmp, c->stream));
+  if (!out_host) return fail(TN_ERR_USAGE, "out is NULL");
+  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, c->d_gather, n_out, c->stream));
+  TN_CUDA(cudaMemcpyAsync(out_host, c->d_gather, n_out * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
   TN_CUDA(cudaStreamSynchronize(c->stream));
   return TN_OK;
 }
