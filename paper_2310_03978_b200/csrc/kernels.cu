@@ -376,12 +376,22 @@ __global__ void __launch_bounds__(256, 3) prep_gt_kernel(const PrepDesc* __restr
 // tile is XOR-swizzled per 16-slot row (mask chosen by the planner) so neither
 // phase has bank conflicts.  All loads of a tile are issued before any use:
 // 32 KB in flight per block, 4 blocks per SM.
+// 16-B global -> shared copy without a register round trip (LDGSTS), L1 bypassed
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 constexpr int BP_TMAX = 4096;
 constexpr size_t BP_SMEM = BP_TMAX * 8 + BP_TMAX / 8 * 8 + 128 * 8 + BP_TMAX * 2 + BP_TMAX / 16;
 
 template <int PLANES>
 __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restrict__ gd,
-                                                         const int64_t* __restrict__ leaf_off) {
+                                                         const int64_t* __restrict__ leaf_off,
+                                                         int bp_cp_async) {
   __shared__ __align__(16) PrepDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
@@ -415,7 +425,14 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
       if ((cc >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
     __syncthreads();   // tables ready / previous tile consumed
     const float2* sp = src + sc;
-    if (vec) {
+    if (vec && bp_cp_async) {   // all 8 x 16-B loads in flight, no register round trip
+#pragma unroll
+      for (int i = 0; i < BP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < T) cp_async16(tile + (e ^ s_m[e >> 4]), sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+      }
+      cp_async_wait_all();
+    } else if (vec) {
       float4 v[BP_TMAX / 512];
 #pragma unroll
       for (int i = 0; i < BP_TMAX / 512; ++i) {
@@ -467,6 +484,7 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
 // 2 K absmax(X) absmax(Y) per real component (bound, no absmax of out exists).
 constexpr int GP_TMAX = 4096;
 constexpr int GP_YMAX = 512, GP_NMAX = 256;
+
 constexpr int GP_BUF = GP_TMAX + GP_TMAX / 32;     // X tile, then (aliased) the padded output tile
 constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX / 8 * 8 /*dst*/ +
                            GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
@@ -475,7 +493,8 @@ constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX 
 // it keeps in registers, so the X tile's smem is reused for the outputs (4 blocks/SM)
 template <int PLANES, int KT>
 __global__ void __launch_bounds__(256, 3) prep_gate_kernel(const PrepDesc* __restrict__ gd,
-                                                           const int64_t* __restrict__ leaf_off) {
+                                                           const int64_t* __restrict__ leaf_off,
+                                                           int gate_cp_async) {
   __shared__ __align__(16) PrepDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
@@ -520,7 +539,14 @@ __global__ void __launch_bounds__(256, 3) prep_gate_kernel(const PrepDesc* __res
       if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
     __syncthreads();   // tables / Y ready, previous tile's outputs consumed
     const float2* sp = src + sc;
-    if (vec) {           // two rounds of 4 x 16-B loads in flight (keeps registers for xs)
+    if (vec && gate_cp_async) {   // all 8 x 16-B loads of the tile in flight, no registers
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < TS) cp_async16(buf + e, sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+      }
+      cp_async_wait_all();
+    } else if (vec) {    // two rounds of 4 x 16-B loads in flight (keeps registers for xs)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float4 v[GP_TMAX / 1024];
@@ -1263,7 +1289,8 @@ cudaError_t launch_gate_t(const PrepDesc* d_desc, int g, const int64_t* leaf_off
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  prep_gate_kernel<PLANES, KT><<<g, 256, GP_SMEM, s>>>(d_desc, leaf_off);
+  static const int cpa = getenv("TN_GATE_CPASYNC") ? atoi(getenv("TN_GATE_CPASYNC")) : 1;
+  prep_gate_kernel<PLANES, KT><<<g, 256, GP_SMEM, s>>>(d_desc, leaf_off, cpa);
   return cudaGetLastError();
 }
 
@@ -1299,10 +1326,11 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
     }
     const int64_t tiles = total / std::max(tile_T, 1);
     const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
+    static const int bp_cpa = getenv("TN_BP_CPASYNC") ? atoi(getenv("TN_BP_CPASYNC")) : 1;
     if (planes == 4)
-      prep_bp_kernel<4><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off);
+      prep_bp_kernel<4><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off, bp_cpa);
     else
-      prep_bp_kernel<2><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off);
+      prep_bp_kernel<2><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off, bp_cpa);
     return cudaGetLastError();
   }
   if (kind == 2) {   // general transposer, tiles of T <= 4096 elements
