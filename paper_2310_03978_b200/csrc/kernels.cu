@@ -381,6 +381,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -390,8 +394,7 @@ constexpr size_t BP_SMEM = BP_TMAX * 8 + BP_TMAX / 8 * 8 + 128 * 8 + BP_TMAX * 2
 
 template <int PLANES>
 __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restrict__ gd,
-                                                         const int64_t* __restrict__ leaf_off,
-                                                         int bp_cp_async) {
+                                                         const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) PrepDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
@@ -425,38 +428,21 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
       if ((cc >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
     __syncthreads();   // tables ready / previous tile consumed
     const float2* sp = src + sc;
-    if (vec && bp_cp_async) {   // all 8 x 16-B loads in flight, no register round trip
+    // every load of the tile in flight at once, straight to shared memory (LDGSTS)
+    if (vec) {
 #pragma unroll
       for (int i = 0; i < BP_TMAX / 512; ++i) {
         const int e = 2 * (threadIdx.x + i * 256);
         if (e < T) cp_async16(tile + (e ^ s_m[e >> 4]), sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
       }
-      cp_async_wait_all();
-    } else if (vec) {
-      float4 v[BP_TMAX / 512];
-#pragma unroll
-      for (int i = 0; i < BP_TMAX / 512; ++i) {
-        const int e = 2 * (threadIdx.x + i * 256);
-        if (e < T) v[i] = __ldg(reinterpret_cast<const float4*>(sp + s_src[e & 63] + s_src[64 + (e >> 6)]));
-      }
-#pragma unroll
-      for (int i = 0; i < BP_TMAX / 512; ++i) {
-        const int e = 2 * (threadIdx.x + i * 256);
-        if (e < T) *reinterpret_cast<float4*>(tile + (e ^ s_m[e >> 4])) = v[i];
-      }
     } else {
-      float2 v[BP_TMAX / 256];
 #pragma unroll
       for (int i = 0; i < BP_TMAX / 256; ++i) {
         const int e = threadIdx.x + i * 256;
-        if (e < T) v[i] = __ldg(sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
-      }
-#pragma unroll
-      for (int i = 0; i < BP_TMAX / 256; ++i) {
-        const int e = threadIdx.x + i * 256;
-        if (e < T) tile[e ^ s_m[e >> 4]] = v[i];
+        if (e < T) cp_async8(tile + (e ^ s_m[e >> 4]), sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
       }
     }
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < BP_TMAX / 2048; ++i) {
@@ -492,9 +478,8 @@ constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX 
 // KT = K (gate inputs per output); a thread owns 16/KT carry positions, whose 16 X values
 // it keeps in registers, so the X tile's smem is reused for the outputs (4 blocks/SM)
 template <int PLANES, int KT>
-__global__ void __launch_bounds__(256, 3) prep_gate_kernel(const PrepDesc* __restrict__ gd,
-                                                           const int64_t* __restrict__ leaf_off,
-                                                           int gate_cp_async) {
+__global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __restrict__ gd,
+                                                           const int64_t* __restrict__ leaf_off) {
   __shared__ __align__(16) PrepDesc d;
   copy_desc_to_smem(&d, gd);
   extern __shared__ __align__(16) uint8_t dyn[];
@@ -539,44 +524,21 @@ __global__ void __launch_bounds__(256, 3) prep_gate_kernel(const PrepDesc* __res
       if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
     __syncthreads();   // tables / Y ready, previous tile's outputs consumed
     const float2* sp = src + sc;
-    if (vec && gate_cp_async) {   // all 8 x 16-B loads of the tile in flight, no registers
+    // every load of the tile in flight at once, straight to shared memory (LDGSTS)
+    if (vec) {
 #pragma unroll
       for (int i = 0; i < GP_TMAX / 512; ++i) {
         const int e = 2 * (threadIdx.x + i * 256);
         if (e < TS) cp_async16(buf + e, sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
       }
-      cp_async_wait_all();
-    } else if (vec) {    // two rounds of 4 x 16-B loads in flight (keeps registers for xs)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float4 v[GP_TMAX / 1024];
-#pragma unroll
-        for (int i = 0; i < GP_TMAX / 1024; ++i) {
-          const int e = 2 * (threadIdx.x + (h * GP_TMAX / 1024 + i) * 256);
-          if (e < TS) v[i] = __ldg(reinterpret_cast<const float4*>(sp + s_src[e & 63] + s_src[64 + (e >> 6)]));
-        }
-#pragma unroll
-        for (int i = 0; i < GP_TMAX / 1024; ++i) {
-          const int e = 2 * (threadIdx.x + (h * GP_TMAX / 1024 + i) * 256);
-          if (e < TS) *reinterpret_cast<float4*>(buf + e) = v[i];
-        }
-      }
     } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float2 v[GP_TMAX / 512];
-#pragma unroll
-        for (int i = 0; i < GP_TMAX / 512; ++i) {
-          const int e = threadIdx.x + (h * GP_TMAX / 512 + i) * 256;
-          if (e < TS) v[i] = __ldg(sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
-        }
-#pragma unroll
-        for (int i = 0; i < GP_TMAX / 512; ++i) {
-          const int e = threadIdx.x + (h * GP_TMAX / 512 + i) * 256;
-          if (e < TS) buf[e] = v[i];
-        }
+      for (int i = 0; i < GP_TMAX / 256; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < TS) cp_async8(buf + e, sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
       }
     }
+    cp_async_wait_all();
     __syncthreads();
     float2 xs[CPT][KT];
 #pragma unroll
@@ -1289,8 +1251,7 @@ cudaError_t launch_gate_t(const PrepDesc* d_desc, int g, const int64_t* leaf_off
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  static const int cpa = getenv("TN_GATE_CPASYNC") ? atoi(getenv("TN_GATE_CPASYNC")) : 1;
-  prep_gate_kernel<PLANES, KT><<<g, 256, GP_SMEM, s>>>(d_desc, leaf_off, cpa);
+  prep_gate_kernel<PLANES, KT><<<g, 256, GP_SMEM, s>>>(d_desc, leaf_off);
   return cudaGetLastError();
 }
 
@@ -1314,7 +1275,8 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
   const int th = 256;
   if (kind == 5) {   // gate-folded prep (K = 1, 2, 4, 8 or 16, carried in the descriptor)
     const int64_t tiles = total / std::max(tile_T, 1);
-    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 3);
+    static const int bps = getenv("TN_GATE_BPS") ? atoi(getenv("TN_GATE_BPS")) : 4;
+    const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * bps);
     return launch_gate(d_desc, planes, gate_k, g, leaf_off, s);
   }
   if (kind == 4) {   // bit-permutation transposer, tiles of tile_T <= 4096 elements
@@ -1326,11 +1288,10 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
     }
     const int64_t tiles = total / std::max(tile_T, 1);
     const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
-    static const int bp_cpa = getenv("TN_BP_CPASYNC") ? atoi(getenv("TN_BP_CPASYNC")) : 1;
     if (planes == 4)
-      prep_bp_kernel<4><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off, bp_cpa);
+      prep_bp_kernel<4><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off);
     else
-      prep_bp_kernel<2><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off, bp_cpa);
+      prep_bp_kernel<2><<<g, th, BP_SMEM, s>>>(d_desc, leaf_off);
     return cudaGetLastError();
   }
   if (kind == 2) {   // general transposer, tiles of T <= 4096 elements
