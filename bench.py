@@ -34,7 +34,7 @@ METRIC = "sustained TFLOPS/GPU and time-to-solution (Sycamore m=18 slices) at 1/
 PAPER_M18_TCC = 6.55e20       # paper's whole m=18 job: 2^23 sub-tasks x 7.81e13 flop
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-graph-pass", action="store_true", help="skip the graph-replay timing pass")
     ap.add_argument("--cpu-flops", type=float, default=6e11,
                     help="target T_cc of one oracle sub-slice sample")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def load_workload(args):
@@ -132,9 +132,13 @@ def oracle_sample(w, target_flops, time_cap_s=60.0):
         extra = fine[len(w.sliced):]
     pcs = path_cost(w.net, w.samples, w.path, fine)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    t0 = time.perf_counter()
-    oracle.contract_slice(w.net, w.path, fine, 0, w.samples)
-    dt = time.perf_counter() - t0
+    # every host core for the oracle's BLAS, also under torchrun (which sets
+    # OMP_NUM_THREADS=1 per rank); `cores` reports the thread count actually set
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        oracle.contract_slice(w.net, w.path, fine, 0, w.samples)
+        dt = time.perf_counter() - t0
     return {"flops": pcs.flops_per_slice, "seconds": dt, "cores": threads,
             "sample": f"oracle (numpy complex128 tensordot) on sub-slice 0 of slice 0 of {w.name}: "
                       f"{len(extra)} extra sliced bonds, T_cc {pcs.flops_per_slice:.3g} flop"}
@@ -352,8 +356,34 @@ def run_ours(args):
     return 0
 
 
-def main():
-    args = parse()
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args, argv):
+    """``--gpus N`` (N > 1) outside torchrun: re-launch this script as N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1, exactly as the driver
+    does; returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args, argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

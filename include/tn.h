@@ -17,8 +17,12 @@
  *
  * Conventions
  *   - All host arrays are owned by the caller and copied before a call returns.
- *   - Device memory is owned by the library (cudaMalloc on the context's device),
- *     except the `out` buffer of tn_sum_slices, which the caller owns.
+ *   - Device memory is obtained through the tn_allocator given to tn_create (the
+ *     Python binding passes torch's caching allocator, so the plan's arena, operand
+ *     scratch and fp64 accumulator are torch-managed memory; SURVEY.md §8 b) and is
+ *     owned by the context until tn_destroy / re-planning returns it; with a NULL
+ *     allocator the library uses cudaMalloc / cudaFree.  The `out` buffer of
+ *     tn_sum_slices is the caller's.
  *   - All GPU work is enqueued on the stream given to tn_create; calls that
  *     return device results do not synchronise unless stated.
  *   - Errors: every call returns a tn_status; on failure tn_last_error() returns
@@ -63,9 +67,28 @@ typedef enum {
   TN_PREC_MIXED = 1
 } tn_precision;
 
-/* Create a context bound to CUDA `device`, enqueuing on `cuda_stream`
- * (a cudaStream_t; NULL = legacy default stream).  *out receives the handle. */
-TN_API tn_status tn_create(tn_ctx** out, int device, void* cuda_stream);
+/* Device-memory source of a context (SURVEY.md §8 b "torch caching allocator").
+ *   alloc(bytes, device, cuda_stream, user) returns a device pointer (>= 256-B
+ *     aligned) valid for work on `cuda_stream`, or NULL on failure (the calling
+ *     tn_* function then fails with TN_ERR_RESOURCE);
+ *   free(ptr, bytes, device, cuda_stream, user) returns a block obtained from alloc;
+ *     work already enqueued on cuda_stream may still use it (stream-ordered release,
+ *     as torch's caching allocator provides).
+ * Both may be called from any tn_* call that (re)plans, loads or destroys. */
+typedef struct {
+  void* (*alloc)(size_t bytes, int device, void* cuda_stream, void* user);
+  void (*free)(void* ptr, size_t bytes, int device, void* cuda_stream, void* user);
+  void* user;
+} tn_allocator;
+
+/* Create a context bound to CUDA `device`, enqueuing on `cuda_stream` (a
+ * cudaStream_t; NULL = legacy default stream).  One context per GPU / rank: "each
+ * A100 GPU executed partial sub-tasks independently".  `allocator`
+ * (copied; NULL = cudaMalloc) supplies every device allocation of the context.
+ * device = -1 creates a host-only planner (bookkeeping and tn_plan_json only).
+ * *out receives the handle.  TN_ERR_USAGE: out NULL, bad device index, an allocator
+ * missing alloc or free; TN_ERR_CUDA: the device is not sm_100. */
+TN_API tn_status tn_create(tn_ctx** out, int device, const tn_allocator* allocator, void* cuda_stream);
 
 /* Load a tensor network (§2.1) and its sparse-state boundary.
  *   n_tensors       number of tensors N (>= 1)
@@ -91,11 +114,13 @@ TN_API tn_status tn_load_network(tn_ctx* ctx, int32_t n_tensors, const int32_t* 
                           int32_t n_open, const int64_t* open_labels,
                           int64_t n_samples, const uint8_t* samples);
 
-/* Replace the tensor values of the loaded network (same layout as `data` above,
- * host pointer) without re-planning: host->device copy on the context stream.  If any
- * leaf's max |Re|,|Im| grows, the fp16-plane delayed-scaling history restarts and the
- * next slice runs unfused; otherwise the history and the captured CUDA
- * graph are kept. */
+/* Replace the tensor values of the loaded network (§2.1: gates and states
+ * as tensors; same layout as `data` above, host pointer) without re-planning:
+ * host->device copy on the context stream.  If any leaf's max |Re|,|Im| changes by
+ * more than 2x (up or down), the fp16-plane delayed-scaling history restarts and
+ * the next slice runs unfused; otherwise the history and the captured
+ * CUDA graph are kept.  TN_ERR_USAGE before tn_load_network or on a host-only
+ * context. */
 TN_API tn_status tn_upload_tensors(tn_ctx* ctx, const double* data);
 
 /* Set the contraction path (§3.1): n_steps = N-1 pairs (i, j) of tensor
@@ -113,8 +138,9 @@ TN_API tn_status tn_set_slices(tn_ctx* ctx, int32_t n_sliced, const int64_t* sli
                         int64_t* n_slices_out);
 
 /* Contract slices t = slice_begin .. slice_end-1 (each one full pass over the
- * path) and ADD each slice's root tensor into the context's fp64 accumulator
- * (fused slice-accumulate).  Repeating a range double-counts it.  Asynchronous.
+ * path, every step the pairwise einsum of Eq. 3, sparse merges per Eq. 7
+ * L306-308; the slices are the independent sub-tasks of L293) and ADD each slice's
+ * root tensor into the context's fp64 accumulator (fused slice-accumulate, L497).  Repeating a range double-counts it.  Asynchronous.
  * precision / mixed_topk: see tn_precision.  TN_ERR_DATA if the range is not
  * inside [0, n_slices).  The first slice a context executes runs every kernel
  * launch directly (it tunes the SIMT kernel variants and seeds the delayed
@@ -123,22 +149,29 @@ TN_API tn_status tn_set_slices(tn_ctx* ctx, int32_t n_sliced, const int64_t* sli
 TN_API tn_status tn_contract(tn_ctx* ctx, int64_t slice_begin, int64_t slice_end,
                       tn_precision precision, int32_t mixed_topk);
 
-/* Zero the fp64 accumulator (asynchronous). */
+/* Zero the fp64 accumulator of the slice sum (L497) and the fused-plane overflow
+ * flag (asynchronous).  TN_ERR_USAGE before tn_set_slices. */
 TN_API tn_status tn_reset_accumulator(tn_ctx* ctx);
 
-/* Write the accumulated amplitudes, in the caller's sample order (full state:
- * index order), as complex128 (re, im) into the DEVICE buffer out[2*n_out].
+/* Write the accumulated amplitudes — "the sum of the resulting tensors" (L497) of the
+ * slices contracted so far, i.e. "the amplitudes of sampled bitstrings" (L256) — in
+ * the caller's sample order (full state: index order), as complex128 (re, im) into
+ * the DEVICE buffer out[2*n_out] (caller-owned, >= 16-B aligned).
  * n_out must equal n_samples (or 2^n_open for the full state; 1 when n_open = 0).
- * Synchronises once to read the fused-plane overflow flag: TN_ERR_DATA (and no
- * output) if a producer epilogue's delayed-scaling margin was exceeded, i.e. the
- * accumulated sum may contain saturated fp16 operands (rerun with
- * TN_FUSE_PLANES=0); tn_reset_accumulator clears the flag. */
+ * Asynchronous on the context stream.  The fused-plane overflow flag (a producer
+ * epilogue's delayed-scaling margin exceeded, so the sum may contain saturated fp16
+ * operands) is checked by the gather kernel itself: when it is set, out is filled
+ * with NaN instead of amplitudes, and tn_last_overflow() reports it after a sync
+ * (rerun with TN_FUSE_PLANES=0); tn_reset_accumulator clears the flag.
+ * TN_ERR_USAGE: n_out mismatch, out NULL, before tn_set_slices. */
 TN_API tn_status tn_sum_slices(tn_ctx* ctx, double* out, int64_t n_out);
 
-/* Same as tn_sum_slices but into a HOST buffer; synchronises the stream. */
+/* Same as tn_sum_slices but into a HOST buffer; synchronises the stream and fails
+ * with TN_ERR_DATA (no output) when the fused-plane overflow flag is set. */
 TN_API tn_status tn_sum_slices_host(tn_ctx* ctx, double* out_host, int64_t n_out);
 
-/* Plan facts for reports. */
+/* Plan facts for reports: T_cc (Eq. 4, ops_per_element = 8) and T_mc
+ * (Eq. 5, sizeof_data = 8) summed over the path of one slice. */
 typedef struct {
   int64_t n_slices;          /* Π dims of the sliced bonds                               */
   int64_t n_out;             /* amplitudes returned by tn_sum_slices                     */
@@ -154,14 +187,17 @@ typedef struct {
   int64_t graph_replays;     /* slices executed by replaying the captured per-slice CUDA
                                 graph (every slice after the first; TN_GRAPHS=0 disables) */
 } tn_info;
+/* TN_ERR_USAGE before tn_set_slices. */
 TN_API tn_status tn_get_info(tn_ctx* ctx, tn_info* info);
 
-/* Bit-exact bookkeeping dump (JSON): per step the pair, J/m/n/k, T_cc, T_mc,
- * routing, and the sparse-merge gather tables; root table; slice decode.
+/* Bit-exact bookkeeping dump (JSON): per step the pair (L259-262), J/m/n/k from the
+ * Eq. 3 set rule (L225-228), T_cc (Eq. 4), T_mc (Eq. 5), routing, and the sparse-
+ * merge gather tables (Eq. 7); root table; slice decode (L292-295).
  * Writes at most cap bytes (NUL-terminated if room) and the full length to *len. */
 TN_API tn_status tn_plan_json(tn_ctx* ctx, char* buf, size_t cap, size_t* len);
 
-/* Kernel-family timing inside tn_contract, for the roofline report.
+/* Kernel-family timing inside tn_contract, for the roofline report (SURVEY.md §8 d:
+ * achieved = algorithmic T_cc (Eq. 4) or bytes (Eq. 5) / measured device time).
  * When enabled, CUDA events bracket every launch of each kernel family on the
  * context stream; stats accumulate until reset.  family: 0 = tcgen05 GEMM,
  * 1 = operand prep (permute + scale + hi/lo split), 2 = SIMT einsum, 3 = slice
@@ -181,7 +217,8 @@ TN_API tn_status tn_reset_kernel_stats(tn_ctx* ctx);
 TN_API tn_status tn_get_step_stats(tn_ctx* ctx, int family, int64_t n, double* ms_out);
 
 /* Stand-alone complex GEMM through the same kernels (unit tests, accumulator
- * probes).  Device pointers, complex64 interleaved:
+ * probes): one step of TTGT's GEMM (L248) in the 3xFP16 split of Eq. 8 (L367-377,
+ * L383-386) or 1-pass (L442), batched with gathers as the sparse einsum (L354).  Device pointers, complex64 interleaved:
  *   A[ga][m][k], B[gb][n][k] (both K-contiguous), C[J][m][n];
  *   ia[J], ib[J] (device int32, may be NULL = slab 0) select the A / B slab of
  *   batch j (the gather of a sparse einsum, Eq. 7 / L354).
@@ -191,8 +228,16 @@ TN_API tn_status tn_cgemm(tn_ctx* ctx, const float* A, const float* B, float* C,
                    int64_t J, int64_t m, int64_t n, int64_t k, int64_t ga, int64_t gb,
                    const int32_t* ia, const int32_t* ib, int passes, int force_simt);
 
+/* Thread-local message of the last failing call on this thread (never NULL). */
 TN_API const char* tn_last_error(void);
+/* Library version string (static storage). */
 TN_API const char* tn_version(void);
+/* 1 if a fused producer epilogue of this context saturated an fp16 plane since the
+ * last tn_reset_accumulator (synchronises the context stream), 0 if not, -1 on a bad
+ * or host-only context.  See tn_sum_slices. */
+TN_API int tn_last_overflow(tn_ctx* ctx);
+/* Release every device block (through the allocator) and the context; waits for
+ * the context stream.  NULL is a no-op. */
 TN_API void tn_destroy(tn_ctx* ctx);
 
 #ifdef __cplusplus

@@ -751,14 +751,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
 
 template <int PASSES, int EW, bool PAIR>
 cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
-  static bool attr_set = false;
   const int smem = Cfg<PASSES, PAIR>::SMEM_BYTES + stage_bytes<EW>();
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(cgemm_tcgen05_kernel<PASSES, EW, PAIR>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  const void* kern = reinterpret_cast<const void*>(cgemm_tcgen05_kernel<PASSES, EW, PAIR>);
+  if (cudaError_t e = set_smem_attr(kern, smem)) return e;
   if constexpr (PAIR) {
     // tiles of 256 rows, one per CTA pair (cluster of 2); persistent over the SMs
     GemmArgs p = a;
@@ -767,8 +762,8 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
     int64_t pairs = p.n_tiles < num_sms / 2 ? p.n_tiles : num_sms / 2;
     // a persistent grid must be co-resident (the wave sync waits on every producer):
     // never launch more clusters than can be active at once
-    static int max_clusters = -1;
-    if (max_clusters < 0) {
+    int max_clusters;
+    {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3((unsigned)num_sms);
       q.blockDim = dim3(64 + 32 * EW);
@@ -780,12 +775,7 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
       qa[0].val.clusterDim.z = 1;
       q.attrs = qa;
       q.numAttrs = 1;
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, cgemm_tcgen05_kernel<PASSES, EW, PAIR>, &q) != cudaSuccess || n <= 0) {
-        cudaGetLastError();
-        n = num_sms / 2;
-      }
-      max_clusters = n;
+      max_clusters = max_active_clusters(kern, q, num_sms / 2);
     }
     if (pairs > max_clusters) pairs = max_clusters;
     if (pairs < 1) pairs = 1;
@@ -812,15 +802,6 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
 
 }  // namespace
 
-int gemm_epi_warps() {   // TN_GEMM_EPI = 8 | 16 epilogue warps (single-CTA kernel; pairs use 8)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TN_GEMM_EPI");
-    v = (e && atoi(e) == 16) ? 16 : 8;
-  }
-  return v;
-}
-
 namespace {
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -842,11 +823,6 @@ EncodeTiledFn get_encode() {
 
 }  // namespace
 
-int gemm_pair_min_m() {
-  const char* e = getenv("TN_GEMM_PAIR_MIN_M");
-  return e ? atoi(e) : 512;
-}
-
 bool gemm_pair_ok(const GemmArgs& a, int min_m) {
   // the pair shares one B slab per 256-row tile: grouped merges (slab per 128-row
   // block) stay on the single-CTA kernel
@@ -855,15 +831,14 @@ bool gemm_pair_ok(const GemmArgs& a, int min_m) {
 
 cudaError_t launch_gemm(const GemmArgs& a_in, int passes, int num_sms, cudaStream_t s) {
   GemmArgs a = a_in;
-  static const int narrow_on = getenv("TN_NARROW_MMA") ? atoi(getenv("TN_NARROW_MMA")) : 1;
-  a.narrow = (narrow_on && a.N <= 64) ? 1 : 0;
+  a.narrow = (g_knobs.narrow_mma && a.N <= 64) ? 1 : 0;
   if (a.wave_sync) {
     cudaError_t e = cudaMemsetAsync(a.wave_ctr, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
   }
   if (a.use_pair)
     return passes == 3 ? launch_impl<3, 8, true>(a, num_sms, s) : launch_impl<1, 8, true>(a, num_sms, s);
-  if (gemm_epi_warps() == 16)
+  if (g_knobs.gemm_epi == 16)
     return passes == 3 ? launch_impl<3, 16, false>(a, num_sms, s) : launch_impl<1, 16, false>(a, num_sms, s);
   return passes == 3 ? launch_impl<3, 8, false>(a, num_sms, s) : launch_impl<1, 8, false>(a, num_sms, s);
 }

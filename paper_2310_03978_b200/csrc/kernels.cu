@@ -1215,11 +1215,15 @@ __global__ void einsum_dot_finalize(const EinsumDesc* __restrict__ gd) {
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// flag (nullable): the fused-plane overflow flag; when set the sum may hold saturated
+// fp16 operands, so NaN is written instead (tn_sum_slices stays asynchronous)
 __global__ void gather_out_kernel(const double2* __restrict__ acc, const int32_t* __restrict__ pos,
-                                  double2* __restrict__ out, int64_t n) {
+                                  double2* __restrict__ out, int64_t n, const int* __restrict__ flag) {
+  const bool bad = flag && *flag;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = acc[pos[i]];
+    out[i] = bad ? make_double2(nan, nan) : acc[pos[i]];
 }
 
 int grid_for(int64_t total, int threads) {
@@ -1244,13 +1248,8 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
 
 template <int PLANES, int KT>
 cudaError_t launch_gate_t(const PrepDesc* d_desc, int g, const int64_t* leaf_off, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prep_gate_kernel<PLANES, KT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(prep_gate_kernel<PLANES, KT>), (int)GP_SMEM))
+    return e;
   prep_gate_kernel<PLANES, KT><<<g, 256, GP_SMEM, s>>>(d_desc, leaf_off);
   return cudaGetLastError();
 }
@@ -1275,17 +1274,14 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
   const int th = 256;
   if (kind == 5) {   // gate-folded prep (K = 1, 2, 4, 8 or 16, carried in the descriptor)
     const int64_t tiles = total / std::max(tile_T, 1);
-    static const int bps = getenv("TN_GATE_BPS") ? atoi(getenv("TN_GATE_BPS")) : 4;
+    const int bps = g_knobs.gate_bps;
     const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * bps);
     return launch_gate(d_desc, planes, gate_k, g, leaf_off, s);
   }
   if (kind == 4) {   // bit-permutation transposer, tiles of tile_T <= 4096 elements
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(prep_bp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM);
-      cudaFuncSetAttribute(prep_bp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM);
-      attr = true;
-    }
+    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(planes == 4 ? prep_bp_kernel<4> : prep_bp_kernel<2>),
+                                      (int)BP_SMEM))
+      return e;
     const int64_t tiles = total / std::max(tile_T, 1);
     const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
     if (planes == 4)
@@ -1295,12 +1291,9 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
     return cudaGetLastError();
   }
   if (kind == 2) {   // general transposer, tiles of T <= 4096 elements
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(prep_gt_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
-      cudaFuncSetAttribute(prep_gt_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
-      attr = true;
-    }
+    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(planes == 4 ? prep_gt_kernel<4> : prep_gt_kernel<2>),
+                                      120 * 1024))
+      return e;
     const size_t smem = (size_t)tile_T * (8 + 8 + 8 + 4);
     int64_t tiles = total / std::max(tile_T, 1);
     const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 6);
@@ -1325,19 +1318,12 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
   return cudaGetLastError();
 }
 
-bool tn_vec2_enabled() {   // TN_SKINNY_VEC2=0 disables the paired-lane kernel (tests)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TN_SKINNY_VEC2");
-    v = e ? atoi(e) : 1;
-  }
-  return v != 0;
-}
+bool tn_vec2_enabled() { return g_knobs.skinny_vec2 != 0; }   // TN_SKINNY_VEC2=0: tests
 
 template <typename F>
 cudaError_t allow_big_smem(F* kern) {
   // the staged small operand can exceed the 48 KB default dynamic smem window
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  return set_smem_attr(reinterpret_cast<const void*>(kern), 96 * 1024);
 }
 
 // instantiated (NMAX, VEC, R) combinations keep the accumulators in registers
@@ -1371,14 +1357,11 @@ cudaError_t enable_wide(cudaError_t e) {
   return e;
 }
 
-cudaError_t enable_einsum_smem() {
-  static bool done = false;
-  if (done) return cudaSuccess;
+cudaError_t enable_einsum_smem() {   // set_smem_attr: once per (kernel, device)
   cudaError_t e = cudaSuccess;
   e = enable_skinny<4>(e); e = enable_skinny<8>(e); e = enable_skinny<16>(e);
   e = enable_skinny<32>(e); e = enable_skinny<64>(e);
   e = enable_wide<2>(e); e = enable_wide<4>(e); e = enable_wide<8>(e); e = enable_wide<16>(e);
-  if (e == cudaSuccess) done = true;
   return e;
 }
 
@@ -1403,7 +1386,7 @@ void launch_skinny(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t*
       einsum_skinny_kernel<NMAX, VEC, false, 1, 1><<<grid_for(h.M / VEC, 256), 256, smem, s>>>(d_desc, leaf_off);
       return;
     }
-    static const int rforce = getenv("TN_SKINNY_ROWS") ? atoi(getenv("TN_SKINNY_ROWS")) : 0;
+    const int rforce = g_knobs.skinny_rows;
     const int64_t kl = h.K < 8 ? h.K : 8;
     int R = (int)std::max<int64_t>(1, std::min<int64_t>(4, 16 / (kl * VEC)));
     if (rows) R = rows;
@@ -1449,10 +1432,8 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
                h.K % 2 == 0 && h.a_off % 2 == 0 && tn_vec2_enabled();
   for (int i = 0; i < h.nm && kpair; ++i) kpair = h.m_sa[i] % 2 == 0 || h.m_ext[i] == 1;
   for (int i = 0; i + 1 < h.nk && kpair; ++i) kpair = h.k_sa[i] % 2 == 0;
-  static const int simt_old = getenv("TN_SIMT_OLD") ? atoi(getenv("TN_SIMT_OLD")) : 0;
-  if ((simt_old || variant == 1) && (h.mode == 1 || h.mode == 3) && h.J == 1) {
-    static bool attr = false;
-    if (!attr) {
+  if ((g_knobs.simt_old || variant == 1) && (h.mode == 1 || h.mode == 3) && h.J == 1) {
+    {
       allow_big_smem(einsum_skinny_old_kernel<4, true>); allow_big_smem(einsum_skinny_old_kernel<8, true>);
       allow_big_smem(einsum_skinny_old_kernel<16, true>); allow_big_smem(einsum_skinny_old_kernel<32, true>);
       allow_big_smem(einsum_skinny_old_kernel<64, true>); allow_big_smem(einsum_skinny_old_kernel<4, false>);
@@ -1462,7 +1443,6 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
       allow_big_smem(einsum_skinny2_old_kernel<16, true>); allow_big_smem(einsum_wide_old_kernel<2>);
       allow_big_smem(einsum_wide_old_kernel<4>); allow_big_smem(einsum_wide_old_kernel<8>);
       allow_big_smem(einsum_wide_old_kernel<16>);
-      attr = true;
     }
     if (h.mode == 1) {
       const size_t smem = sizeof(float2) * h.K * h.N + sizeof(int64_t) * h.K;
@@ -1535,8 +1515,8 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
 }
 
 cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
-                              cudaStream_t s) {
-  gather_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(acc, pos, out, n);
+                              const int* flag, cudaStream_t s) {
+  gather_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(acc, pos, out, n, flag);
   return cudaGetLastError();
 }
 
@@ -1562,5 +1542,61 @@ cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_
   if (b < 1) b = 1;
   absmax_kernel<<<(unsigned)b, 256, 0, s>>>(x, n, out);
   return cudaGetLastError();
+}
+}  // namespace tn
+
+// ---------------------------------------------------------------- knobs, per-device attributes
+#include <map>
+#include <mutex>
+namespace tn {
+Knobs g_knobs;
+
+namespace {
+int env_or(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_attr;       // (kernel, device) -> smem bytes set
+std::map<std::pair<const void*, int>, int> g_clusters;   // (kernel, device) -> max clusters
+}  // namespace
+
+void refresh_knobs() {
+  Knobs k;
+  k.gate_bps = env_or("TN_GATE_BPS", 4);
+  k.skinny_rows = env_or("TN_SKINNY_ROWS", 0);
+  k.simt_old = env_or("TN_SIMT_OLD", 0);
+  k.skinny_vec2 = env_or("TN_SKINNY_VEC2", 1);
+  k.narrow_mma = env_or("TN_NARROW_MMA", 1);
+  k.gemm_epi = env_or("TN_GEMM_EPI", 8) == 16 ? 16 : 8;
+  k.prep_bp = env_or("TN_PREP_BP", 1);
+  k.pair_min_m = env_or("TN_GEMM_PAIR_MIN_M", 512);
+  g_knobs = k;
+}
+
+cudaError_t set_smem_attr(const void* kernel, int bytes) {
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_attr.find({kernel, dev});
+  if (it != g_attr.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) g_attr[{kernel, dev}] = bytes;
+  return e;
+}
+
+int max_active_clusters(const void* kernel, const cudaLaunchConfig_t& cfg, int fallback) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fallback;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_clusters.find({kernel, dev});
+  if (it != g_clusters.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = fallback;
+  }
+  g_clusters[{kernel, dev}] = n;
+  return n;
 }
 }  // namespace tn

@@ -132,6 +132,11 @@ struct tn_ctx {
   int device = 0;
   bool host_only = false;   // device = -1: plan/bookkeeping only, no CUDA calls
   cudaStream_t stream = nullptr;
+  // device memory source (SURVEY.md §8 b: the caller's allocator, e.g. torch's caching
+  // allocator); has_alloc = false: cudaMalloc / cudaFree.  owned: live blocks -> bytes
+  tn_allocator alloc{};
+  bool has_alloc = false;
+  std::unordered_map<void*, size_t> owned;
   int num_sms = 148;
   // k-blocks per promoted TMEM chunk: 3-pass / 1-pass
   int kchunk3 = 1, kchunk1 = 0;
@@ -238,6 +243,35 @@ int64_t index_in(const std::vector<uint64_t>& t, uint64_t v) {
   return it - t.begin();
 }
 
+// Device memory of a context: every block comes from the caller's allocator when one
+// was given to tn_create (on the context stream), else from cudaMalloc.
+tn_status mem_alloc(tn_ctx* c, void** p, size_t bytes) {
+  *p = nullptr;
+  if (c->has_alloc) {
+    *p = c->alloc.alloc(bytes, c->device, reinterpret_cast<void*>(c->stream), c->alloc.user);
+    if (!*p) return fail(TN_ERR_RESOURCE, "allocator returned NULL for " + std::to_string(bytes) + " bytes");
+  } else {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      *p = nullptr;
+      return fail(TN_ERR_RESOURCE, "device allocation of " + std::to_string(bytes) + " bytes failed");
+    }
+    if (e != cudaSuccess) return fail(TN_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  c->owned[*p] = bytes;
+  return TN_OK;
+}
+
+void mem_free(tn_ctx* c, void* p) {
+  if (!p) return;
+  auto it = c->owned.find(p);
+  const size_t bytes = it == c->owned.end() ? 0 : it->second;
+  if (it != c->owned.end()) c->owned.erase(it);
+  if (c->has_alloc) c->alloc.free(p, bytes, c->device, reinterpret_cast<void*>(c->stream), c->alloc.user);
+  else cudaFree(p);
+}
+
 void free_dev(tn_ctx* c) {
   if (c->host_only) { c->planned = false; return; }
   if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
@@ -247,8 +281,7 @@ void free_dev(tn_ctx* c) {
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
                   c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt,
                   c->d_hist, c->d_pexp, c->d_flag, c->d_wave, c->d_gather};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  for (void* p : ptrs) mem_free(c, p);
   c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
   c->d_absmax = nullptr; c->d_scales = nullptr; c->d_leaf_off = nullptr; c->d_counter = nullptr;
   c->d_out_pos = nullptr; c->d_slice_desc = nullptr; c->d_terms_i = nullptr; c->d_terms_s = nullptr;
@@ -263,12 +296,10 @@ void free_dev(tn_ctx* c) {
 template <typename T>
 tn_status dev_alloc(tn_ctx* c, T** p, size_t count) {
   size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
-  if (e == cudaErrorMemoryAllocation) {
-    cudaGetLastError();
-    return fail(TN_ERR_RESOURCE, "device allocation of " + std::to_string(bytes) + " bytes failed");
-  }
-  if (e != cudaSuccess) return fail(TN_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  void* q = nullptr;
+  tn_status st = mem_alloc(c, &q, bytes);
+  if (st) return st;
+  *p = reinterpret_cast<T*>(q);
   c->device_bytes += bytes;
   return TN_OK;
 }
@@ -594,8 +625,7 @@ bool plan_gate(tn::PrepDesc& p, const tn::EinsumDesc& e, std::vector<int64_t>& t
 int choose_prep_kind(tn::PrepDesc& p, int force, std::vector<int64_t>& tab) {
   if (force == 0 || force == 1) return force;
   if (force != 2 && force != 4 && p.nk > 0 && p.k_s[p.nk - 1] == 1 && p.k_ext[p.nk - 1] % 8 == 0) return 1;
-  static const int bp_on = getenv("TN_PREP_BP") ? atoi(getenv("TN_PREP_BP")) : 1;
-  if (force != 2 && (bp_on || force == 4) && plan_bp(p, tab)) return 4;
+  if (force != 2 && (tn::g_knobs.prep_bp || force == 4) && plan_bp(p, tab)) return 4;
   if (p.K % 8 != 0 || p.Kpad != p.K || (force != 2 && p.G * p.R * p.K < 2048))
     return p.read_r_fast ? 0 : 1;
   struct D { int64_t e, s, t; };
@@ -781,7 +811,7 @@ tn_status build_plan(tn_ctx* c) {
   const int group_mode = env_int("TN_GROUP", 1);          // 0 off, 1 cost model, 2 always
   const double group_max_bytes = 1e9 * env_int("TN_GROUP_MAX_GB", 32);
   const int group_min_use = env_int("TN_GROUP_MIN_USE", 8);   // route when useful >= 1/this
-  const int pair_min_m = tn::gemm_pair_min_m();            // CTA-pair GEMM for M >= this
+  const int pair_min_m = tn::g_knobs.pair_min_m;            // CTA-pair GEMM for M >= this
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
   const int dense_mode = env_int("TN_DENSE_MERGE", 1);     // 0 off, 1 cost rule, 2 always (tests)
@@ -1728,7 +1758,7 @@ tn_status build_plan(tn_ctx* c) {
         // 16-B plane vectors: the 8 lowest column indices must be plane-contiguous
         const bool cols = !qo.empty() && qo.back().second == 1 && qo.back().first >= 3;
         const bool rows = fuse_planes != 2 && !po.empty() && po.back().second == 1 && po.back().first >= 3 &&
-                          pp.gemm.M % 8 == 0 && (pp.gemm.use_pair || tn::gemm_epi_warps() == 8);
+                          pp.gemm.M % 8 == 0 && (pp.gemm.use_pair || tn::g_knobs.gemm_epi == 8);
         if (pp.gemm.N % 8 != 0 || (!cols && !rows)) {
           skip("no plane-contiguous run of 8 rows or columns");
           continue;
@@ -2044,7 +2074,12 @@ tn_status build_leaves(tn_ctx* c) {
 
 tn_status upload_leaves(tn_ctx* c, const double* data) {
   if (!c->h_leaf_pinned) TN_CUDA(cudaMallocHost(&c->h_leaf_pinned, std::max<int64_t>(c->leaf_elems, 1) * sizeof(float2)));
-  if (!c->d_leaf) TN_CUDA(cudaMalloc(&c->d_leaf, std::max<int64_t>(c->leaf_elems, 1) * sizeof(float2)));
+  if (!c->d_leaf) {
+    void* q = nullptr;
+    tn_status st = mem_alloc(c, &q, std::max<int64_t>(c->leaf_elems, 1) * sizeof(float2));
+    if (st) return st;
+    c->d_leaf = reinterpret_cast<float2*>(q);
+  }
   // the previous upload may still be in flight from the pinned buffer
   TN_CUDA(cudaStreamSynchronize(c->stream));
   c->leaf_absmax.assign(c->n_tensors, 0.f);
@@ -2090,9 +2125,12 @@ extern "C" {
 const char* tn_last_error(void) { return g_err.c_str(); }
 const char* tn_version(void) { return "tn-b200 0.1 (sm_100a tcgen05)"; }
 
-tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
+tn_status tn_create(tn_ctx** out, int device, const tn_allocator* allocator, void* cuda_stream) {
   if (!out) return fail(TN_ERR_USAGE, "out is NULL");
   *out = nullptr;
+  if (allocator && (!allocator->alloc || !allocator->free))
+    return fail(TN_ERR_USAGE, "tn_allocator needs both alloc and free");
+  tn::refresh_knobs();
   if (device == -1) {
     tn_ctx* c = new tn_ctx();
     c->host_only = true;
@@ -2111,6 +2149,7 @@ tn_status tn_create(tn_ctx** out, int device, void* cuda_stream) {
   tn_ctx* c = new tn_ctx();
   c->device = device;
   c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  if (allocator) { c->alloc = *allocator; c->has_alloc = true; }
   c->num_sms = prop.multiProcessorCount;
   c->kchunk3 = env_int("TN_KCHUNK3", 1);
   // 1-pass: whole K in TMEM (promoting every 4 k-blocks costs 10 % and only moves the
@@ -2132,8 +2171,9 @@ void tn_destroy(tn_ctx* c) {
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   free_dev(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  if (c->d_leaf) cudaFree(c->d_leaf);
+  mem_free(c, c->d_leaf);
   if (c->h_leaf_pinned) cudaFreeHost(c->h_leaf_pinned);
+  for (auto& kv : std::unordered_map<void*, size_t>(c->owned)) mem_free(c, kv.first);
   delete c;
 }
 
@@ -2219,7 +2259,7 @@ tn_status tn_load_network(tn_ctx* c, int32_t n_tensors, const int32_t* ranks, co
     c->loaded = true;
     return TN_OK;
   }
-  if (c->d_leaf) { cudaFree(c->d_leaf); c->d_leaf = nullptr; }
+  if (c->d_leaf) { cudaStreamSynchronize(c->stream); mem_free(c, c->d_leaf); c->d_leaf = nullptr; }
   if (c->h_leaf_pinned) { cudaFreeHost(c->h_leaf_pinned); c->h_leaf_pinned = nullptr; }
   st = upload_leaves(c, data);
   if (st) return st;
@@ -2234,13 +2274,16 @@ tn_status tn_upload_tensors(tn_ctx* c, const double* data) {
   const std::vector<float> before = c->leaf_absmax;
   tn_status st = upload_leaves(c, data);
   if (st) return st;
-  bool grew = before.size() != c->leaf_absmax.size();
-  for (size_t t = 0; t < before.size() && !grew; ++t) grew = c->leaf_absmax[t] > before[t];
-  if (c->planned && c->d_hist && grew) {
-    // a leaf got larger: restart the delayed-scaling history; the next slice runs
-    // unfused and re-seeds it (SIMT variants and the captured graph are kept).  Values
-    // no larger than before keep the history (the 32x margin and the overflow check
-    // cover the slice-to-slice variation).
+  // a leaf's absmax moved by more than 2x: restart the delayed-scaling history; the
+  // next slice runs unfused and re-seeds it (SIMT variants and the captured graph are
+  // kept).  Growth would eat the 32x margin; a shrink would leave the history (a
+  // running max) stale-large, the planes' exponent too low and the fp16 lo plane
+  // (then hi) in subnormals.  Smaller changes keep the history (the margin and the
+  // overflow check cover the slice-to-slice variation).
+  bool moved = before.size() != c->leaf_absmax.size();
+  for (size_t t = 0; t < before.size() && !moved; ++t)
+    moved = c->leaf_absmax[t] > 2.f * before[t] || 2.f * c->leaf_absmax[t] < before[t];
+  if (c->planned && c->d_hist && moved) {
     TN_CUDA(cudaMemsetAsync(c->d_hist, 0, c->steps.size() * sizeof(unsigned), c->stream));
     c->tuned = false;
   }
@@ -2326,10 +2369,12 @@ tn_status check_plane_overflow(tn_ctx* c) {
 tn_status tn_sum_slices(tn_ctx* c, double* out, int64_t n_out) {
   tn_status st = check_planned(c);
   if (st) return st;
-  if ((st = check_plane_overflow(c))) return st;
   if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
   if (!out) return fail(TN_ERR_USAGE, "out is NULL");
-  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, reinterpret_cast<double2*>(out), n_out, c->stream));
+  TN_CUDA(cudaSetDevice(c->device));
+  // asynchronous: the gather itself turns a set overflow flag into NaN output
+  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, reinterpret_cast<double2*>(out), n_out, c->d_flag,
+                                c->stream));
   return TN_OK;
 }
 
@@ -2339,10 +2384,20 @@ tn_status tn_sum_slices_host(tn_ctx* c, double* out_host, int64_t n_out) {
   if ((st = check_plane_overflow(c))) return st;
   if (n_out != c->n_out) return fail(TN_ERR_USAGE, "n_out must be " + std::to_string(c->n_out));
   if (!out_host) return fail(TN_ERR_USAGE, "out is NULL");
-  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, c->d_gather, n_out, c->stream));
+  TN_CUDA(tn::launch_gather_out(c->d_acc, c->d_out_pos, c->d_gather, n_out, nullptr, c->stream));
   TN_CUDA(cudaMemcpyAsync(out_host, c->d_gather, n_out * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
   TN_CUDA(cudaStreamSynchronize(c->stream));
   return TN_OK;
+}
+
+int tn_last_overflow(tn_ctx* c) {
+  if (!c || c->host_only || !c->planned) return -1;
+  if (cudaSetDevice(c->device) != cudaSuccess) return -1;
+  int flag = 0;
+  if (cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return -1;
+  return flag ? 1 : 0;
 }
 
 tn_status tn_get_info(tn_ctx* c, tn_info* info) {
@@ -2482,8 +2537,9 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
   cudaStream_t sm = c->stream;
   unsigned* am = nullptr;
   int* sc = nullptr;
-  TN_CUDA(cudaMalloc(&am, 16));
-  TN_CUDA(cudaMalloc(&sc, 16));
+  tn_status st0 = mem_alloc(c, reinterpret_cast<void**>(&am), 16);
+  if (!st0) st0 = mem_alloc(c, reinterpret_cast<void**>(&sc), 16);
+  if (st0) { mem_free(c, am); return st0; }
   TN_CUDA(cudaMemsetAsync(am, 0, 16, sm));
   const float2* A2 = reinterpret_cast<const float2*>(A);
   const float2* B2 = reinterpret_cast<const float2*>(B);
@@ -2502,17 +2558,17 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     e.nk = 1; e.k_ext[0] = k; e.k_sa[0] = 1; e.k_sb[0] = 1;
     fill_shifts(e);
     tn::EinsumDesc* d = nullptr;
-    TN_CUDA(cudaMalloc(&d, sizeof(e)));
+    if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&d), sizeof(e))) return st1;
     TN_CUDA(cudaMemcpyAsync(d, &e, sizeof(e), cudaMemcpyHostToDevice, sm));
     TN_CUDA(tn::launch_einsum(d, e, nullptr, sm));
     TN_CUDA(cudaStreamSynchronize(sm));
-    cudaFree(d);
+    mem_free(c, d);
   } else {
     const int64_t Kpad = (k + 7) / 8 * 8;
     const int64_t b0 = (4 * ga * m * Kpad * 2 + 1023) / 1024 * 1024;
     const int64_t b1 = (4 * gb * n * Kpad * 2 + 1023) / 1024 * 1024;
     uint8_t* scr = nullptr;
-    TN_CUDA(cudaMalloc(&scr, b0 + b1));
+    if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&scr), b0 + b1)) return st1;
     tn::PrepDesc p[2];
     tn::GemmArgs g;
     memset(&g, 0, sizeof(g));
@@ -2533,12 +2589,12 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
       p[side].scale_out = sc + side;
       if (!tn::encode_plane_map(side ? &g.mapB : &g.mapA, p[side].dst, Kpad, R, G, 4, 128, err, sizeof(err)) ||
           (side == 1 && !tn::encode_plane_map(&g.mapB2, p[side].dst, Kpad, R, G, 4, 64, err, sizeof(err)))) {
-        cudaFree(scr);
+        mem_free(c, scr);
         return fail(TN_ERR_INTERNAL, err);
       }
     }
     tn::PrepDesc* dp = nullptr;
-    TN_CUDA(cudaMalloc(&dp, sizeof(p)));
+    if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&dp), sizeof(p))) return st1;
     TN_CUDA(cudaMemcpyAsync(dp, p, sizeof(p), cudaMemcpyHostToDevice, sm));
     const int planes = passes == 3 ? 4 : 2;
     TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, 0, 0, nullptr, sm));
@@ -2553,8 +2609,9 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * J;
     g.kchunk = passes == 3 ? c->kchunk3 : c->kchunk1;
     g.group_m = c->group_m;
-    g.use_pair = tn::gemm_pair_ok(g, tn::gemm_pair_min_m()) ? 1 : 0;
-    if (!c->d_wave) TN_CUDA(cudaMalloc(&c->d_wave, sizeof(unsigned long long)));
+    g.use_pair = tn::gemm_pair_ok(g, tn::g_knobs.pair_min_m) ? 1 : 0;
+    if (!c->d_wave)
+      if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&c->d_wave), sizeof(unsigned long long))) return st1;
     g.wave_ctr = c->d_wave;
     g.wave_sync = (env_int("TN_WAVE_SYNC", 1) && k >= 1024) ? 1 : 0;
     {
@@ -2562,12 +2619,12 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
       TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));
     }
     cudaError_t e = cudaStreamSynchronize(sm);
-    cudaFree(dp);
-    cudaFree(scr);
+    mem_free(c, dp);
+    mem_free(c, scr);
     if (e != cudaSuccess) result = fail(TN_ERR_CUDA, std::string("cgemm: ") + cudaGetErrorString(e));
   }
-  cudaFree(am);
-  cudaFree(sc);
+  mem_free(c, am);
+  mem_free(c, sc);
   return result;
 }
 

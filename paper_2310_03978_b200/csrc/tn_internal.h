@@ -156,6 +156,28 @@ struct SliceDesc {
   unsigned* hist; int* pexp;
 };
 
+// Process-wide tuning and test-forcing knobs of the kernel launchers, re-read from the
+// TN_* environment at every tn_create (DESIGN.md §10 lists every knob; planner knobs
+// are read per plan in build_plan).  Defaults are the product settings.
+struct Knobs {
+  int gate_bps = 4;       // TN_GATE_BPS: gate-folded prep blocks per SM
+  int skinny_rows = 0;    // TN_SKINNY_ROWS: force the skinny kernel's rows per thread (tests)
+  int simt_old = 0;       // TN_SIMT_OLD: force the previous skinny design (A/B tests)
+  int skinny_vec2 = 1;    // TN_SKINNY_VEC2=0: no paired-lane / k-pair 16-B accesses (tests)
+  int narrow_mma = 1;     // TN_NARROW_MMA=0: N <= 64 GEMMs issue N = 128 MMAs (A/B tests)
+  int gemm_epi = 8;       // TN_GEMM_EPI: 8 or 16 epilogue warps on single-CTA GEMMs
+  int prep_bp = 1;        // TN_PREP_BP=0: no bit-permutation transposer (A/B tests)
+  int pair_min_m = 512;   // TN_GEMM_PAIR_MIN_M: CTA-pair GEMM from this M (0 = never)
+};
+extern Knobs g_knobs;
+void refresh_knobs();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device context: applied once
+// per (kernel, device), thread-safe; a later larger request raises it
+cudaError_t set_smem_attr(const void* kernel, int bytes);
+// cudaOccupancyMaxActiveClusters of a launch configuration, cached per (kernel, device)
+int max_active_clusters(const void* kernel, const cudaLaunchConfig_t& cfg, int fallback);
+
 // kernel launchers (kernels.cu / gemm_tcgen05.cu)
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
 cudaError_t launch_set_counter(int64_t* counter, int64_t value, cudaStream_t s);
@@ -166,14 +188,12 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
                           const int64_t* leaf_off, cudaStream_t s, int variant = 0);
 int einsum_variants(const EinsumDesc& host_desc);
 cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
-                              cudaStream_t s);
+                              const int* flag, cudaStream_t s);
 cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s);
-// CTA-pair eligibility: M >= min_m (TN_GEMM_PAIR_MIN_M, default 512; 0 = never) and
+// CTA-pair eligibility: M >= min_m (g_knobs.pair_min_m, default 512; 0 = never) and
 // one B slab per 256-row tile (not a grouped merge)
 bool gemm_pair_ok(const GemmArgs& a, int min_m);
-int gemm_pair_min_m();                   // reads TN_GEMM_PAIR_MIN_M
-int gemm_epi_warps();                    // reads TN_GEMM_EPI (8 or 16)
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
                       int planes, int box_rows, char* err, size_t errcap);
 

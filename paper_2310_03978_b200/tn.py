@@ -24,7 +24,8 @@ _STATUS = {0: "TN_OK", 1: "TN_ERR_USAGE", 2: "TN_ERR_DATA", 3: "TN_ERR_RESOURCE"
 SYMBOLS = ["tn_create", "tn_load_network", "tn_upload_tensors", "tn_set_path", "tn_set_slices",
            "tn_contract", "tn_reset_accumulator", "tn_sum_slices", "tn_sum_slices_host",
            "tn_get_info", "tn_plan_json", "tn_set_profiling", "tn_get_kernel_stats",
-           "tn_reset_kernel_stats", "tn_get_step_stats", "tn_cgemm", "tn_last_error", "tn_version", "tn_destroy"]
+           "tn_reset_kernel_stats", "tn_get_step_stats", "tn_cgemm", "tn_last_error", "tn_version",
+           "tn_last_overflow", "tn_destroy"]
 
 
 class TNLibraryError(RuntimeError):
@@ -46,6 +47,36 @@ class Info(C.Structure):
                 ("graph_replays", C.c_int64)]
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    """tn_allocator (include/tn.h)."""
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", C.c_void_p)]
+
+
+def _torch_alloc(nbytes, device, stream, user):
+    """tn_allocator.alloc -> torch's CUDA caching allocator on the context stream."""
+    try:
+        import torch
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device=int(device), stream=int(stream or 0))
+    except Exception:  # noqa: BLE001  (out of memory -> NULL -> TN_ERR_RESOURCE)
+        return None
+
+
+def _torch_free(ptr, nbytes, device, stream, user):
+    try:
+        import torch
+        torch.cuda.caching_allocator_delete(int(ptr))
+    except Exception:  # noqa: BLE001  (interpreter shutdown)
+        pass
+
+
+# one process-wide pair of callbacks (ctypes keeps them alive while referenced here)
+_TORCH_ALLOCATOR = Allocator(ALLOC_FN(_torch_alloc), FREE_FN(_torch_free), None)
+
+
 class KernelStats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
                 ("bytes", C.c_double)]
@@ -55,20 +86,25 @@ _lib = None
 
 
 def lib():
-    """Load libtn.so (building it first if sources are newer and nvcc exists)."""
+    """Load libtn.so, (re)building it first when it is missing or older than its
+    sources and nvcc exists; a present library is used as is when nvcc is absent."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        try:
-            from . import _build
-            _build.build()
-        except Exception as e:  # noqa: BLE001
-            raise TNLibraryError(f"libtn.so missing and could not be built: {e}") from e
+    from . import _build
+    if _build.needs_build():
+        have_nvcc = os.path.exists(_build.NVCC)
+        if have_nvcc:
+            try:
+                _build.build()
+            except Exception as e:  # noqa: BLE001
+                raise TNLibraryError(f"libtn.so could not be built: {e}") from e
+        elif not os.path.exists(LIB_PATH):
+            raise TNLibraryError(f"libtn.so missing and nvcc not found at {_build.NVCC}")
     L = C.CDLL(LIB_PATH)
     P, I32, I64, D, VP = C.POINTER, C.c_int32, C.c_int64, C.c_double, C.c_void_p
     sig = {
-        "tn_create": [P(VP), C.c_int, VP],
+        "tn_create": [P(VP), C.c_int, P(Allocator), VP],
         "tn_load_network": [VP, I32, VP, VP, VP, VP, I32, VP, I64, VP],
         "tn_upload_tensors": [VP, VP],
         "tn_set_path": [VP, I32, VP],
@@ -89,6 +125,8 @@ def lib():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = C.c_int
+    L.tn_last_overflow.argtypes = [VP]
+    L.tn_last_overflow.restype = C.c_int
     L.tn_last_error.restype = C.c_char_p
     L.tn_version.restype = C.c_char_p
     L.tn_destroy.argtypes = [VP]
@@ -118,18 +156,32 @@ def _tptr(t):
 class Contraction:
     """One context = one device + stream (``tn_create``)."""
 
-    def __init__(self, device: int = 0, stream=None):
-        """device = -1 builds a host-only planner (bookkeeping, no execution)."""
+    def __init__(self, device: int = 0, stream=None, allocator: str = "torch"):
+        """device = -1 builds a host-only planner (bookkeeping, no execution).
+        ``stream``: a torch.cuda.Stream (kept as ``self.stream``; every call of this
+        context is enqueued on it), a raw cudaStream_t int, or None (legacy stream).
+        ``allocator``: "torch" = every device allocation of the context comes from
+        torch's caching allocator (tn_allocator callbacks); "cuda" = cudaMalloc."""
         L = lib()
         h = C.c_void_p()
         s = None
         if stream is not None:
             s = C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
-        _check(L.tn_create(C.byref(h), int(device), s))
+        if allocator not in ("torch", "cuda"):
+            raise ValueError("allocator must be 'torch' or 'cuda'")
+        a = C.byref(_TORCH_ALLOCATOR) if allocator == "torch" and device >= 0 else None
+        _check(L.tn_create(C.byref(h), int(device), a, s))
+        self.allocator = allocator
         self._h = h
         self.device = device
+        self.stream = stream if stream is not None and not isinstance(stream, int) else None
         self.n_slices = None
         self.n_out = None
+
+    @property
+    def torch_device(self):
+        import torch
+        return torch.device("cuda", self.device) if self.device >= 0 else torch.device("cpu")
 
     def close(self):
         if getattr(self, "_h", None):
@@ -186,6 +238,13 @@ class Contraction:
     def sum_slices(self, out):
         """Write amplitudes into a complex128 CUDA torch tensor of length n_out."""
         _check(lib().tn_sum_slices(self._h, _tptr(out), int(self.n_out)))
+
+    def overflow(self) -> bool:
+        """tn_last_overflow: a fused epilogue saturated an fp16 plane (synchronises)."""
+        v = lib().tn_last_overflow(self._h)
+        if v < 0:
+            raise TNError(1, "tn_last_overflow: bad or host-only context")
+        return bool(v)
 
     def sum_slices_host(self, out: np.ndarray | None = None) -> np.ndarray:
         if out is None:

@@ -140,3 +140,19 @@ def test_error_codes():
     with pytest.raises(TNError) as e:
         c2.load_network(ranks, labels, dims, data, opens, smp)
     assert e.value.status == 2
+
+
+def test_create_rejects_incomplete_allocator():
+    """tn_create validates the tn_allocator (SURVEY.md §8 b) before touching a device:
+    an allocator without a free callback is a usage error."""
+    import ctypes as C
+    L = tnlib.lib()
+    h = C.c_void_p()
+    half = tnlib.Allocator(tnlib.ALLOC_FN(lambda n, d, s, u: None), tnlib.FREE_FN(), None)
+    assert L.tn_create(C.byref(h), -1, C.byref(half), None) == 1
+    assert b"alloc and free" in L.tn_last_error()
+    full = tnlib.Allocator(tnlib.ALLOC_FN(lambda n, d, s, u: None),
+                           tnlib.FREE_FN(lambda p, n, d, s, u: None), None)
+    assert L.tn_create(C.byref(h), -1, C.byref(full), None) == 0
+    L.tn_destroy(h)
+    assert L.tn_last_overflow(None) == -1

@@ -21,10 +21,15 @@ def main():
     ap.add_argument("--workload", default="c4")
     ap.add_argument("--slices", type=int, default=2)
     ap.add_argument("--precision", default="extended")
+    ap.add_argument("--boundary", default="single", help="c4 boundary: single | sparse16")
+    ap.add_argument("--peak", type=int, default=32)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from tnworkloads import configs
-    w = {"c4": configs.c4, "c3": configs.c3, "c2": configs.c2}[a.workload]()
+    if a.workload == "c4":
+        w = configs.c4(a.boundary, a.peak)
+    else:
+        w = {"c3": configs.c3, "c2": configs.c2}[a.workload]()
     stream = torch.cuda.Stream()
     ctx = Contraction(0, stream)
     ctx.setup(w.net, w.samples, w.path, w.sliced)
