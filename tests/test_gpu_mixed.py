@@ -1,0 +1,103 @@
+"""Mixed precision at full width (``-m gpu``): the Table 3 analogue (§4.3
+L471-490) and the Fig. 8 analogue (error against the number of contracted slices,
+L456-463) on Sycamore-53 m=18 sub-networks (the bench's C4 orders with extra bonds
+fixed so that the CPU oracle can afford them).
+
+* top-k sweep: the k tensor-core steps with the largest T_cc run 1-pass fp16
+  (TN_PREC_MIXED), k in {0, 1, 10, all}; k = 0 is the extended path (<= 1e-5), every
+  mixed setting <= 5e-3 (BASELINE.json), and the error grows with k (more steps
+  lose the lo planes) — the monotone trend of Table 3.
+* slices: relative L2 and eps_L2^2 (Eq. 9) of the running slice sum after each of
+  16 sub-slices, for the extended and mixed paths: stays within the bars at every
+  prefix (errors of independent slices do not accumulate into a bias)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle                                          # noqa: E402
+from tnworkloads import configs                        # noqa: E402
+from tnworkloads.network import fix_bonds              # noqa: E402
+from tnworkloads.treesa import refine_slices           # noqa: E402
+from paper_2310_03978_b200 import Contraction          # noqa: E402
+
+EXT_TOL, MIX_TOL = 1e-5, 5e-3
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def eps_l2sq(a, b):
+    """Eq. 9: relative error of the squared L2 norm."""
+    nb = float(np.sum(np.abs(b) ** 2))
+    return abs(float(np.sum(np.abs(a) ** 2)) - nb) / nb
+
+
+def _dump(name, doc):
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, name), "w") as f:
+        json.dump(doc, f, indent=1)
+
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("boundary", ["single", "sparse16"])
+def test_topk_sweep_c4_subnetwork(boundary):
+    w = configs.c4(boundary)
+    fine, _ = refine_slices(w.net, w.samples, w.path, w.sliced, 3e11, max_extra=48)
+    sub = fix_bonds(w.net, {x: 0 for x in fine[len(w.sliced):]})
+    ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(sub, w.samples, w.path, w.sliced)
+    steps = c.plan_json()["steps"]
+    tc = sorted((s["tcc"] for s in steps if s["route"] == "tcgen05"), reverse=True)
+    total = sum(s["tcc"] for s in steps)
+    rows = []
+    for k in (0, 1, 10, len(tc)):
+        c.reset_accumulator()
+        c.contract(0, 1, "extended" if k == 0 else "mixed", k)
+        got = c.sum_slices_host()
+        rows.append({"k": k, "tcc_ratio": sum(tc[:k]) / total, "rel_l2": rel_l2(got, ref),
+                     "eps_l2sq": eps_l2sq(got, ref)})
+    c.close()
+    _dump(f"topk_sweep_{boundary}.json", {"workload": w.name, "n_tc_steps": len(tc), "rows": rows})
+    print(f"[topk {boundary}] " + "  ".join(f"k={r['k']}: {r['rel_l2']:.2e}" for r in rows))
+    assert rows[0]["rel_l2"] <= EXT_TOL
+    for r in rows[1:]:
+        assert r["rel_l2"] <= MIX_TOL, r
+    errs = [r["rel_l2"] for r in rows]
+    assert errs[0] < errs[1] < errs[2], errs          # monotone over the steps that matter
+    assert errs[3] >= 0.95 * errs[2], errs            # the tail adds little, never removes
+
+
+@pytest.mark.timeout(1200)
+def test_error_against_number_of_slices():
+    w = configs.c4("sparse16")
+    fine, _ = refine_slices(w.net, w.samples, w.path, w.sliced, 3e10, max_extra=48)
+    extra = fine[len(w.sliced):]
+    assert len(extra) > 4
+    sub = fix_bonds(w.net, {x: 0 for x in extra[4:]})
+    sliced = list(w.sliced) + extra[:4]                 # 16 sub-slices of slice 0
+    refs = [oracle.contract_slice(sub, w.path, sliced, t, w.samples) for t in range(16)]
+    run_ref = np.cumsum(np.stack(refs), axis=0)
+    doc = {"workload": w.name, "sub_slices": 16, "rows": []}
+    for prec, tol in (("extended", EXT_TOL), ("mixed", MIX_TOL)):
+        c = Contraction(device=0, stream=torch.cuda.current_stream())
+        c.setup(sub, w.samples, w.path, sliced)
+        for t in range(16):
+            c.contract(t, t + 1, prec, 10)
+            got = c.sum_slices_host()
+            doc["rows"].append({"precision": prec, "slices": t + 1, "rel_l2": rel_l2(got, run_ref[t]),
+                                "eps_l2sq": eps_l2sq(got, run_ref[t])})
+        c.close()
+    _dump("error_vs_slices.json", doc)
+    for prec, tol in (("extended", EXT_TOL), ("mixed", MIX_TOL)):
+        e = [r["rel_l2"] for r in doc["rows"] if r["precision"] == prec]
+        print(f"[slices {prec}] " + " ".join(f"{x:.1e}" for x in e))
+        assert max(e) <= tol, (prec, e)
+        assert e[-1] <= 2.0 * max(e[:4]), (prec, e)     # no drift with the number of slices
