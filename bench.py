@@ -41,7 +41,10 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c4", "c3", "c2"])
-    ap.add_argument("--boundary", default="single")
+    # headline: the paper's sampling boundary (2^16 uniform samples) with
+    # per-slice intermediates up to 2^32 elements (32 GiB: sized for 180 GB of HBM3e;
+    # DESIGN.md §3 "Why peak 2^32"); --boundary single is the secondary line
+    ap.add_argument("--boundary", default="sparse16")
     ap.add_argument("--peak", type=int, default=32)
     ap.add_argument("--order-tag", default="a64", help="order file variant (tools/make_orders.py)")
     ap.add_argument("--precision", default="extended", choices=["extended", "mixed"])

@@ -39,13 +39,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     bdir = os.path.join(HERE, "build")
     os.makedirs(bdir, exist_ok=True)
     procs = []
+    headers = glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "tn.h")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
     for src in sources():
         obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if (not force and os.path.exists(obj) and
+                os.path.getmtime(obj) > max(os.path.getmtime(src), newest_header)):
+            continue   # object newer than its source and every header
         cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))
-        objs.append(obj)
     for p, src in procs:
         out, _ = p.communicate()
         if p.returncode != 0:

@@ -27,14 +27,18 @@
 // matrix of the batched GEMM" of L354 become TMA slab coordinates, so no
 // gathered copies are materialised.
 //
-// Structure (one CTA per SM, persistent, 10 warps):
+// Structure (one CTA per SM, persistent, 12 warps = 3 warpgroups):
 //   warp 0      TMA producer: 4D tensor-map loads (K, rows, slab, plane), box
 //               32x128, SWIZZLE_64B, into a STAGES-deep smem ring (mbarrier tx).
 //   warp 1      TMEM allocator (512 cols) + single-thread tcgen05.mma issuer,
 //               kind::f16, M=128 N=128 K=16; a chunk accumulator Cr|Ci is 256
 //               TMEM columns, double-buffered; tcgen05.commit frees smem stages
 //               and hands finished chunks to the epilogue.
-//   warps 2-9   epilogue: warp (quadrant q, half h) owns TMEM lanes 32q..32q+31
+//   warps 2-3   idle (they complete warpgroup 0, whose register budget is lowered
+//               to 40 per thread with setmaxnreg so that the two epilogue
+//               warpgroups can raise theirs to 232: the epilogue's 64+64 fp32
+//               column sums and a 32+32-column TMEM load fit without spills)
+//   warps 4-11  epilogue: warp (quadrant q, half h) owns TMEM lanes 32q..32q+31
 //               and output columns 64h..64h+63 of both Cr and Ci; tcgen05.ld
 //               32x32b.x32 -> fp32 RN register sums of the chunks scaled by
 //               2^-(sA+sB) and store complex64 (or fused fp64 accumulate into the
@@ -230,8 +234,12 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int64_t tile, int
   }
 }
 
+constexpr int EPI_WARP0 = 4;   // first epilogue warp (warpgroup 1)
+constexpr int REG_LOW = 40, REG_HIGH = 232;   // setmaxnreg budgets: warpgroup 0 / epilogue
+
 template <int PASSES, int EW, bool PAIR>
-__global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
+__global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
+  static_assert(EW == 8, "two epilogue warpgroups");
   using C = Cfg<PASSES, PAIR>;
   constexpr int PLANES = C::PLANES, STAGES = C::STAGES;
   // narrow GEMMs (N <= 64): N = 64 MMAs (half the tensor work of the padded 128-wide
@@ -292,6 +300,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // register split (per SM sub-partition: REG_LOW + 2 x REG_HIGH <= 512 per lane slot);
+  // each role's code sits inside the branch that set its budget, so ptxas allocates it
+  // under that budget
+  if (warp < EPI_WARP0) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_LOW));
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------------- TMA producer
@@ -442,13 +455,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
         }
       }
     }
+  }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 2..)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_HIGH));
+    // ---------------------------------------------------------------- epilogue (warps 4..11)
     // warp (quadrant q, sub s) owns TMEM lanes 32q..32q+31 and WC output columns
     // WC*s .. WC*s+WC-1 of both Cr and Ci (WC = 64 with 8 warps, 32 with 16)
     constexpr int WC = 512 / EW;
     const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - EPI_WARP0) >> 2;
     const int row = quad * 32 + lane;
     const float scale = ldexpf(1.0f, -(*args.scaleA + *args.scaleB));
     // fused plane output: consumer exponent sC = max(bound, delayed scaling); the planes
@@ -457,7 +472,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
     if (args.out_planes) {
       const int sab = *args.scaleA + *args.scaleB;
       plane_sc = max(sab + args.plane_exp, *args.plane_pexp);
-      if (blockIdx.x == 0 && threadIdx.x == 64) *args.plane_scale_out = plane_sc;
+      if (blockIdx.x == 0 && threadIdx.x == 32 * EPI_WARP0) *args.plane_scale_out = plane_sc;
     }
     bool plane_ovf = false;
     float amax = 0.f;
@@ -509,7 +524,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
       if (args.out_gen) {
         // ---- general output map: column offsets of this tile into smem, then stores
         int64_t* tab = noff_tab + (titer & 1) * BN;
-        const int et = threadIdx.x - 64;                 // epilogue thread 0 .. 32*EW-1
+        const int et = threadIdx.x - 32 * EPI_WARP0;     // epilogue thread 0 .. 32*EW-1
         if (et < BN) {
           int64_t t = (int64_t)nt * BN + et, off = 0;
           for (int q = args.n_qo - 1; q >= 0; --q) {
@@ -540,7 +555,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1) cgemm_tcgen05_kernel(const __
               // unit-stride plane dim = the 8 lowest row bits: stage 8 columns of the
               // warp's 32 rows in smem, then lane (group g, column c) writes rows
               // 8g..8g+7 of column c as one 16-B vector per plane
-              float2* buf = stage_buf + (warp - 2) * 32 * 9;
+              float2* buf = stage_buf + (warp - EPI_WARP0) * 32 * 9;
               const int g = lane >> 3, cc = lane & 7;
               const int64_t gb = __shfl_sync(0xffffffffu, rb, 8 * g);
 #pragma unroll
@@ -766,7 +781,7 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
     {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3((unsigned)num_sms);
-      q.blockDim = dim3(64 + 32 * EW);
+      q.blockDim = dim3(32 * EPI_WARP0 + 32 * EW);
       q.dynamicSmemBytes = smem;
       cudaLaunchAttribute qa[1];
       qa[0].id = cudaLaunchAttributeClusterDimension;
@@ -781,7 +796,7 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
     if (pairs < 1) pairs = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * pairs));
-    cfg.blockDim = dim3(64 + 32 * EW);
+    cfg.blockDim = dim3(32 * EPI_WARP0 + 32 * EW);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -795,7 +810,7 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
   } else {
     int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
     if (grid < 1) grid = 1;
-    cgemm_tcgen05_kernel<PASSES, EW, PAIR><<<(unsigned)grid, 64 + 32 * EW, smem, s>>>(a);
+    cgemm_tcgen05_kernel<PASSES, EW, PAIR><<<(unsigned)grid, 32 * EPI_WARP0 + 32 * EW, smem, s>>>(a);
     return cudaGetLastError();
   }
 }
@@ -838,8 +853,6 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int passes, int num_sms, cudaStrea
   }
   if (a.use_pair)
     return passes == 3 ? launch_impl<3, 8, true>(a, num_sms, s) : launch_impl<1, 8, true>(a, num_sms, s);
-  if (g_knobs.gemm_epi == 16)
-    return passes == 3 ? launch_impl<3, 16, false>(a, num_sms, s) : launch_impl<1, 16, false>(a, num_sms, s);
   return passes == 3 ? launch_impl<3, 8, false>(a, num_sms, s) : launch_impl<1, 8, false>(a, num_sms, s);
 }
 

@@ -1568,7 +1568,6 @@ void refresh_knobs() {
   k.simt_old = env_or("TN_SIMT_OLD", 0);
   k.skinny_vec2 = env_or("TN_SKINNY_VEC2", 1);
   k.narrow_mma = env_or("TN_NARROW_MMA", 1);
-  k.gemm_epi = env_or("TN_GEMM_EPI", 8) == 16 ? 16 : 8;
   k.prep_bp = env_or("TN_PREP_BP", 1);
   k.pair_min_m = env_or("TN_GEMM_PAIR_MIN_M", 512);
   g_knobs = k;

@@ -183,6 +183,11 @@ struct tn_ctx {
   // gate folding decided by a previous planning pass: the folded step's output is not
   // allocated and its inputs stay live until its consumer's prep has read them
   std::vector<char> fold_hint;
+  // index reordering (§4.1): 2 = every step's output in its consumer's
+  // order (the generalised look-ahead, default), 1 = the paper's top-k rule (Fig. 3),
+  // 0 = none (every output in Eq. 3's natural [J][P][Q] order); TN_REORDER / _TOPK
+  int reorder_mode = 2, reorder_topk = 10;
+  std::vector<char> reorder_sel, reorder_mod;   // mode 1: selected / modified steps
   std::vector<int32_t> out_pos;
   int64_t n_out = 0, acc_elems = 1;
   double flops_per_slice = 0, tc_flops = 0, bytes_per_slice = 0, peak = 0;
@@ -794,6 +799,73 @@ int env_int(const char* name, int dflt) {
 
 // ---------------------------------------------------------------- planning
 
+// The paper's top-k index-reordering rule (§4.1, Fig. 3), on a label
+// replay of the path: (1) rank all contractions by T_cc (Eq. 4; ties: earlier step
+// first), keep the top k; (2) a contraction qualifies when no reordering has modified
+// it (its [J][P][Q] output is then GEMM-form, so reordering its inputs alone makes it a
+// GEMM); (3) the contractions that produced its two inputs ("associated", L337) must
+// not have been modified either (a leaf input has none); (4) reorder: the current and
+// the associated contractions are marked modified.  Sets c->reorder_sel / reorder_mod.
+void paper_reorder(tn_ctx* c, const std::unordered_map<int, View>& live0, int topk) {
+  const int n_steps = (int)c->path.size();
+  struct T { std::vector<std::pair<int64_t, int64_t>> d; std::vector<int> q; int64_t G = 1; int prod = -1; };
+  std::unordered_map<int, T> st;
+  for (auto& kv : live0) {
+    T t;
+    for (auto& d : kv.second.dims) if (d.label != GROUP) t.d.push_back({d.label, d.ext});
+    t.q = kv.second.q;
+    t.G = kv.second.has_group() ? (int64_t)kv.second.table.size() : 1;
+    st[kv.first] = t;
+  }
+  std::vector<unsigned __int128> w(n_steps);   // J*m*n*k (T_cc / 8), exact
+  std::vector<std::array<int, 2>> prod(n_steps);
+  for (int s = 0; s < n_steps; ++s) {
+    T& A = st[c->path[s].first];
+    T& B = st[c->path[s].second];
+    prod[s] = {A.prod, B.prod};
+    unsigned __int128 m = 1, n = 1, k = 1, J = 1;
+    T out;
+    for (auto& a : A.d) {
+      bool shared = false;
+      for (auto& b : B.d) shared = shared || b.first == a.first;
+      if (shared) k *= (unsigned __int128)a.second; else { m *= (unsigned __int128)a.second; out.d.push_back(a); }
+    }
+    for (auto& b : B.d) {
+      bool shared = false;
+      for (auto& a : A.d) shared = shared || a.first == b.first;
+      if (!shared) { n *= (unsigned __int128)b.second; out.d.push_back(b); }
+    }
+    if (!A.q.empty() && !B.q.empty()) {
+      out.q = A.q;
+      out.q.insert(out.q.end(), B.q.begin(), B.q.end());
+      std::sort(out.q.begin(), out.q.end());
+      out.G = (int64_t)table_for(c, out.q).size();
+      J = (unsigned __int128)out.G;
+    } else if (!A.q.empty()) {
+      m *= (unsigned __int128)A.G; out.q = A.q; out.G = A.G;
+    } else if (!B.q.empty()) {
+      n *= (unsigned __int128)B.G; out.q = B.q; out.G = B.G;
+    }
+    w[s] = J * m * n * k;
+    out.prod = s;
+    st.erase(c->path[s].second);
+    st[c->path[s].first] = out;
+  }
+  std::vector<int> rank(n_steps);
+  std::iota(rank.begin(), rank.end(), 0);
+  std::stable_sort(rank.begin(), rank.end(), [&](int a, int b) { return w[a] > w[b]; });
+  for (int r = 0; r < std::min(topk, n_steps); ++r) {
+    const int s = rank[r];
+    if (c->reorder_mod[s]) continue;                              // (2) modified already
+    bool ok = true;
+    for (int p : prod[s]) if (p >= 0 && c->reorder_mod[p]) ok = false;
+    if (!ok) continue;                                            // (3) an associated one is
+    c->reorder_sel[s] = 1;                                        // (4) reorder
+    c->reorder_mod[s] = 1;
+    for (int p : prod[s]) if (p >= 0) c->reorder_mod[p] = 1;
+  }
+}
+
 tn_status build_plan(tn_ctx* c) {
   free_dev(c);
   c->device_bytes = c->leaf_elems * sizeof(float2);
@@ -879,6 +951,17 @@ tn_status build_plan(tn_ctx* c) {
       lab[j].clear();
       producer[i] = s;
     }
+  }
+  // Which producers write their output in the consumer's order (index reordering).
+  c->reorder_mode = env_int("TN_REORDER", 2);
+  c->reorder_topk = env_int("TN_REORDER_TOPK", 10);
+  c->reorder_sel.assign(n_steps, 0);
+  c->reorder_mod.assign(n_steps, 0);
+  if (c->reorder_mode == 1) paper_reorder(c, live, c->reorder_topk);
+  for (int s = 0; s < n_steps; ++s) {
+    const bool keep = c->reorder_mode == 2 ||
+                      (c->reorder_mode == 1 && consumer_step[s] >= 0 && c->reorder_sel[consumer_step[s]]);
+    if (!keep) consumer_k[s].clear();
   }
   // stable partition: bonds the consumer keeps first, bonds it contracts last (sorted)
   auto consumer_order = [](std::vector<VDim>& d, const std::unordered_set<int64_t>& kc) {
@@ -1758,7 +1841,7 @@ tn_status build_plan(tn_ctx* c) {
         // 16-B plane vectors: the 8 lowest column indices must be plane-contiguous
         const bool cols = !qo.empty() && qo.back().second == 1 && qo.back().first >= 3;
         const bool rows = fuse_planes != 2 && !po.empty() && po.back().second == 1 && po.back().first >= 3 &&
-                          pp.gemm.M % 8 == 0 && (pp.gemm.use_pair || tn::g_knobs.gemm_epi == 8);
+                          pp.gemm.M % 8 == 0;
         if (pp.gemm.N % 8 != 0 || (!cols && !rows)) {
           skip("no plane-contiguous run of 8 rows or columns");
           continue;
@@ -2452,7 +2535,16 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     }
     o += "}";
   }
-  o += "],\"out_pos\":";
+  o += "],\"reorder\":{\"mode\":" + std::to_string(c->reorder_mode) + ",\"topk\":" +
+       std::to_string(c->reorder_topk) + ",\"selected\":[";
+  bool first = true;
+  for (size_t s = 0; s < c->reorder_sel.size(); ++s)
+    if (c->reorder_sel[s]) { o += (first ? "" : ",") + std::to_string(s); first = false; }
+  o += "],\"modified\":[";
+  first = true;
+  for (size_t s = 0; s < c->reorder_mod.size(); ++s)
+    if (c->reorder_mod[s]) { o += (first ? "" : ",") + std::to_string(s); first = false; }
+  o += "]},\"out_pos\":";
   json_u64_list(o, c->out_pos);
   char b[256];
   snprintf(b, sizeof(b), ",\"flops_per_slice\":%.17g,\"tc_flops_per_slice\":%.17g,\"peak_elements\":%.17g}",

@@ -165,7 +165,6 @@ struct Knobs {
   int simt_old = 0;       // TN_SIMT_OLD: force the previous skinny design (A/B tests)
   int skinny_vec2 = 1;    // TN_SKINNY_VEC2=0: no paired-lane / k-pair 16-B accesses (tests)
   int narrow_mma = 1;     // TN_NARROW_MMA=0: N <= 64 GEMMs issue N = 128 MMAs (A/B tests)
-  int gemm_epi = 8;       // TN_GEMM_EPI: 8 or 16 epilogue warps on single-CTA GEMMs
   int prep_bp = 1;        // TN_PREP_BP=0: no bit-permutation transposer (A/B tests)
   int pair_min_m = 512;   // TN_GEMM_PAIR_MIN_M: CTA-pair GEMM from this M (0 = never)
 };

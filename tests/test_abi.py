@@ -156,3 +156,49 @@ def test_create_rejects_incomplete_allocator():
     assert L.tn_create(C.byref(h), -1, C.byref(full), None) == 0
     L.tn_destroy(h)
     assert L.tn_last_overflow(None) == -1
+
+
+@pytest.mark.parametrize("topk", [1, 3, 10, 1000])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_paper_reorder_selection_matches_oracle(topk, seed, monkeypatch):
+    """f3: the library's TN_REORDER=1 pass (§4.1 top-k rule) selects and marks
+    exactly the steps the oracle's plain implementation of the rule does, on T_cc the
+    oracle re-derives itself (Eq. 4)."""
+    from oracle.reorder import paper_topk_reorder
+    monkeypatch.setenv("TN_REORDER", "1")
+    monkeypatch.setenv("TN_REORDER_TOPK", str(topk))
+    w = configs.small(grid=(3, 4), cycles=8, mode=["sparse", "single", "full"][seed], n_samples=64,
+                      n_slices=4, seed=seed)
+    c, pj = _check_plan(w)
+    bk = oracle.plan_bookkeeping(w.net, w.path, w.sliced, w.samples)
+    sel, mod = paper_topk_reorder(w.path, len(w.net.labels), [r["tcc"] for r in bk], topk)
+    assert pj["reorder"]["mode"] == 1
+    assert pj["reorder"]["selected"] == sel and pj["reorder"]["modified"] == mod
+    assert sel, "the rule selects at least the top contraction"
+
+
+def test_paper_reorder_selection_c4(monkeypatch):
+    from oracle.reorder import paper_topk_reorder
+    monkeypatch.setenv("TN_REORDER", "1")
+    w = configs.c4("single", 32, "a64")
+    c = Contraction(device=-1)
+    c.setup(w.net, w.samples, w.path, w.sliced)
+    pj = c.plan_json()
+    tcc = [s["tcc"] for s in pj["steps"]]
+    sel, mod = paper_topk_reorder(w.path, len(w.net.labels), tcc, 10)
+    assert pj["reorder"]["selected"] == sel and pj["reorder"]["modified"] == mod
+    # the reordered producers are exactly the associated contractions: only they write
+    # the consumer's order (out_gen); in mode 0 no producer does
+    assert 1 <= len(sel) <= 10
+
+
+def test_reorder_modes_change_layout_not_bookkeeping(monkeypatch):
+    w = configs.small(grid=(3, 4), cycles=8, mode="sparse", n_samples=64, n_slices=4, seed=0)
+    for k, v in {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2"}.items():
+        monkeypatch.setenv(k, v)
+    gens = {}
+    for mode in (0, 1, 2):
+        monkeypatch.setenv("TN_REORDER", str(mode))
+        c, pj = _check_plan(w)
+        gens[mode] = sum(1 for s in pj["steps"] if s["out_gen"])
+    assert gens[0] == 0 and gens[0] <= gens[1] <= gens[2] and gens[2] > 0

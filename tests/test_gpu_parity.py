@@ -168,6 +168,11 @@ ROUTES = {
                       "TN_OUT_LAYOUT": "0"},
     "tc_ungrouped": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
                      "TN_GROUP": "0"},
+    # index reordering (§4.1): the paper's top-k rule, and none at all
+    "tc_reorder_paper": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                         "TN_REORDER": "1", "TN_REORDER_TOPK": "4"},
+    "tc_reorder_none": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
+                        "TN_REORDER": "0"},
     "default": {},
 }
 

@@ -326,3 +326,43 @@ def test_sparse_merge_bookkeeping_equals_naive_loop_count(seed):
             assert rec["ia"] == nv["ia"] and rec["ib"] == nv["ib"]
     assert n_merge >= 2, n_merge          # the J > 1 branch is exercised
     assert oracle.plan_bookkeeping(net, path, (), smp)[-1]["J"] == len(np.unique(smp, axis=0))
+
+
+# ----------------------------------------------------------------------------- §4.1 reorder rule (f3)
+# Hand-worked cases of the Fig. 3 rule on the Fig. 1(b)-shaped tree
+# M = einsum(I, J) [s0], N = einsum(K, L) [s1], O = einsum(M, N) [s2], final (O, P) [s3];
+# expected sets derived by hand from the four steps of the rule, not by running it.
+_FIG1B_PATH = [(0, 1), (2, 3), (0, 2), (0, 4)]
+
+
+def test_reorder_producers_follow_stable_ids():
+    from oracle.reorder import producers
+    assert producers(_FIG1B_PATH, 5) == [(None, None), (None, None), (0, 1), (2, None)]
+
+
+@pytest.mark.parametrize("tcc,k,selected,modified", [
+    # O ranks first: O and its associated M, N are reordered; the final step's associated
+    # contraction O is modified -> skipped; M and N are modified -> skipped
+    ([10, 20, 100, 50], 4, [2], [0, 1, 2]),
+    # N first (leaf inputs only); O's associated N is modified -> skipped; the final step's
+    # associated O is untouched -> reordered (O modified); M has leaf inputs -> reordered
+    ([10, 200, 100, 50], 4, [0, 1, 3], [0, 1, 2, 3]),
+    # top-2 group {N, O}: only N
+    ([10, 200, 100, 50], 2, [1], [1]),
+    # equal T_cc: earlier step first (reading R18): s0, s1, then s2 blocked, s3 reordered
+    ([5, 5, 5, 5], 4, [0, 1, 3], [0, 1, 2, 3]),
+    # k = 0: nothing
+    ([10, 20, 100, 50], 0, [], []),
+])
+def test_reorder_rule_hand_worked(tcc, k, selected, modified):
+    from oracle.reorder import paper_topk_reorder
+    assert paper_topk_reorder(_FIG1B_PATH, 5, tcc, k) == (selected, modified)
+
+
+def test_reorder_rule_chain_blocks_consumers_of_reordered_steps():
+    # chain X=(0,1) s0, Y=(0,2) s1, Z=(0,3) s2: Y ranks first -> Y, X modified; Z's
+    # associated Y is modified -> skipped; X is modified -> skipped
+    from oracle.reorder import paper_topk_reorder
+    assert paper_topk_reorder([(0, 1), (0, 2), (0, 3)], 4, [1, 9, 5], 3) == ([1], [0, 1])
+    # Z first -> Z, Y modified; then Y skipped; X: its inputs are leaves -> reordered
+    assert paper_topk_reorder([(0, 1), (0, 2), (0, 3)], 4, [1, 5, 9], 3) == ([0, 2], [0, 1, 2])

@@ -71,6 +71,11 @@ class Tree:
         return v
 
     alpha = 0.0     # Eq. 6 memory weight: flop-equivalents per byte of T_mc (8 B/element)
+    # balanced-index feedback (App. A.2): a GEMM with k < 64 or min(m, n) < 32
+    # under-uses the tensor cores ("k should be equal to or greater than 64 ... m or n
+    # should be greater than or equal to 32"); beta weights the lost tensor time,
+    # T_cc * (1/u - 1) with u = min(1, k/64) * min(1, min(m, n)/32), into the score
+    beta = 0.0
 
     def pair_cost(self, La, Qa, Lb, Qb, keep):
         """(cost, log2 out size) of contracting (La,Qa) with (Lb,Qb); keep = ~sliced.
@@ -90,6 +95,10 @@ class Tree:
             ln += ub
         out = (La ^ Lb).bit_count() + self.log2U(Qa | Qb)
         cost = 2.0 ** (lj + lm + ln + lk + 3.0)
+        if self.beta:
+            lu = min(0.0, lk - 6.0) + min(0.0, min(lm, ln) - 5.0)   # log2 u
+            if lu < 0.0:
+                cost += self.beta * cost * (2.0 ** -lu - 1.0)
         if self.alpha:
             cost += self.alpha * 8.0 * (2.0 ** (La.bit_count() + ua) + 2.0 ** (Lb.bit_count() + ub)
                                         + 2.0 ** out)
@@ -207,14 +216,16 @@ def refine_slices(net, samples, path, sliced, target_flops: float, max_extra: in
 
 def optimize(net, samples, path0, peak_log2: float, seed: int = 0, sweeps: int = 40,
              fine_sweeps: int = 6, t0: float = 0.3, t1: float = 0.01, max_slices: int = 64,
-             cand_top: int = 48, log=None, alpha: float = 0.0):
+             cand_top: int = 48, log=None, alpha: float = 0.0, beta: float = 0.0):
     """SA on the unsliced tree, then dynamic slicing down to ``peak_log2`` with a
     short low-temperature re-tune after every cut.  The score is Eq. 6's
-    T_cc + alpha*T_mc (alpha in flop per byte).  Returns (path, sliced labels,
+    T_cc + alpha*T_mc (alpha in flop per byte), plus the App. A.2 balance term with
+    weight beta (Tree.beta).  Returns (path, sliced labels,
     per-slice cost, peak log2)."""
     rng = np.random.default_rng(seed)
     tr = Tree(net, samples, path0)
     tr.alpha = alpha
+    tr.beta = beta
     full = (1 << len(tr.label_of)) - 1
     tr.anneal(full, sweeps, t0, t1, None, rng)
     sliced_bits = []

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--boundary", default="single")
     ap.add_argument("--alpha", type=float, default=0.0,
                     help="Eq. 6 memory weight (flop-equivalents per byte of T_mc)")
+    ap.add_argument("--beta", type=float, default=0.0,
+                    help="App. A.2 balanced-index feedback weight (tnworkloads.treesa.Tree.beta)")
     ap.add_argument("--tag", default="")
     ap.add_argument("--cycles", type=int, default=18)
     args = ap.parse_args()
@@ -34,7 +36,8 @@ def main():
         t = time.time()
         p0 = bisection_path(w.net, w.samples, seed=3004 + s, leaf_size=8, time_weight=0.3)
         path, sliced, tot, pk = optimize(w.net, w.samples, p0, args.peak, seed=3004 + s,
-                                         sweeps=args.sweeps, alpha=args.alpha)
+                                         sweeps=args.sweeps, alpha=args.alpha,
+                                         beta=args.beta)
         pc = path_cost(w.net, w.samples, path, sliced)
         score = tot * 2.0 ** len(sliced)
         print(f"seed {s}: per-slice {pc.flops_per_slice:.3g} peak 2^{pc.peak_log2:.1f} "
@@ -44,7 +47,8 @@ def main():
             best = (path, sliced, pc, s, score)
     path, sliced, pc, s, score = best
     meta = {"method": "bisection(KL, time_weight 0.3) + tree SA + dynamic slicing",
-            "score": "Eq. 6 T_cc + alpha*T_mc", "alpha": args.alpha,
+            "score": "Eq. 6 T_cc + alpha*T_mc (+ beta * App. A.2 balance term)", "alpha": args.alpha,
+            "beta": args.beta,
             "seed": 3004 + s, "peak_log2_target": args.peak, "sweeps": args.sweeps,
             "flops_per_slice": pc.flops_per_slice, "peak_log2": pc.peak_log2,
             "n_sliced": len(sliced), "boundary": args.boundary}
