@@ -223,10 +223,13 @@ TN_API tn_status tn_get_step_stats(tn_ctx* ctx, int family, int64_t n, double* m
  *   ia[J], ib[J] (device int32, may be NULL = slab 0) select the A / B slab of
  *   batch j (the gather of a sparse einsum, Eq. 7 / L354).
  *   passes = 3 (hi/lo split) or 1; force_simt != 0 runs the SIMT kernel instead.
- * Synchronous on the context stream. */
+ *   format = operand format of the tensor-core path (Fig. 4):
+ *   0 fp16 (the product path), 1 bf16 (3xBF16 / 1xBF16), 2 tf32 (3xTF32 of Eq. 8 as
+ *   printed / 1xTF32, kind::tf32); formats 1 and 2 run single-CTA tiles.
+ * Synchronous on the context stream.  TN_ERR_USAGE on bad sizes, passes or format. */
 TN_API tn_status tn_cgemm(tn_ctx* ctx, const float* A, const float* B, float* C,
                    int64_t J, int64_t m, int64_t n, int64_t k, int64_t ga, int64_t gb,
-                   const int32_t* ia, const int32_t* ib, int passes, int force_simt);
+                   const int32_t* ia, const int32_t* ib, int passes, int force_simt, int format);
 
 /* Thread-local message of the last failing call on this thread (never NULL). */
 TN_API const char* tn_last_error(void);

@@ -22,6 +22,13 @@
 // round-to-nearest: the bias becomes ≈0.37·2^-24·(MMAs per chunk) independently
 // of K, and the chunk sums combine without bias.
 //
+// Operand formats (template FMT, Fig. 4): fp16 planes (the product
+// path), bf16 planes (3xBF16, L383) or tf32 in 32-bit containers (3xTF32, Eq. 8 as
+// printed, kind::tf32).  A k-block is always 64 B of K per row (32 fp16/bf16 or 16
+// tf32 elements) and an MMA consumes 32 B of it, so the smem layout, descriptors and
+// issue order are the same for all three; only the instruction kind, the descriptor's
+// operand-format fields and the TMA element type differ.
+//
 // Sparse einsum (Eq. 7) is the same kernel: batch j selects the A and
 // B slabs through the gather tables ia/ib — the "separate pointers for each
 // matrix of the batched GEMM" of L354 become TMA slab coordinates, so no
@@ -50,6 +57,9 @@ namespace tn {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 32;          // BK in complex k (64 B fp16 rows)
+enum { FMT_F16 = 0, FMT_BF16 = 1, FMT_TF32 = 2 };
+// k elements per 64-B k-block row
+template <int FMT> __host__ __device__ constexpr int bk_elems() { return FMT == FMT_TF32 ? 16 : 32; }
 constexpr int PLANE_TILE = 128 * BK * 2;            // 8 KiB per plane tile
 constexpr uint32_t TMEM_COLS = 512;
 
@@ -72,13 +82,14 @@ struct Cfg {
 template <int EW>
 constexpr int stage_bytes() { return EW == 8 ? EW * 32 * 9 * 8 : 0; }
 
-// instruction descriptor, kind::f16: D=f32 (bits 4-5 = 1), A=B=f16, K-major,
-// N>>3 at bits 17-22, M>>4 at bits 24-28; bit 13 = negate A.
-template <bool PAIR>
+// instruction descriptor: D=f32 (bits 4-5 = 1), A/B format at bits 7-9 / 10-12 (kind::f16:
+// 0 = f16, 1 = bf16; kind::tf32: 2 = tf32), K-major, N>>3 at bits 17-22, M>>4 at bits
+// 24-28; bit 13 = negate A.
+template <bool PAIR, int FMT = FMT_F16>
 struct Idesc {
-  static constexpr uint32_t POS = (1u << 4) | ((uint32_t)(BN >> 3) << 17) |
+  static constexpr uint32_t AB = FMT == FMT_F16 ? 0u : (FMT == FMT_BF16 ? 1u : 2u);
+  static constexpr uint32_t POS = (1u << 4) | (AB << 7) | (AB << 10) | ((uint32_t)(BN >> 3) << 17) |
                                   ((uint32_t)((PAIR ? 2 * BM : BM) >> 4) << 24);
-  static constexpr uint32_t NEG = POS | (1u << 13);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -157,10 +168,21 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
 // MMA issue: called by the whole (converged) MMA warp; one lane is elected inside
 // the asm, so every operand stays warp-uniform (uniform registers, no per-MMA
 // ELECT / R2UR.BROADCAST loop as when a single-lane branch issues it).
-template <bool PAIR>
+template <bool PAIR, int FMT = FMT_F16>
 __device__ __forceinline__ void mma_t(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                       uint32_t accumulate) {
-  if constexpr (PAIR)
+  if constexpr (FMT == FMT_TF32) {
+    if constexpr (PAIR)
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+          "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+    else
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+          "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  } else if constexpr (PAIR)
     asm volatile(
         "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
         "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
@@ -237,15 +259,16 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int64_t tile, int
 constexpr int EPI_WARP0 = 4;   // first epilogue warp (warpgroup 1)
 constexpr int REG_LOW = 40, REG_HIGH = 232;   // setmaxnreg budgets: warpgroup 0 / epilogue
 
-template <int PASSES, int EW, bool PAIR>
+template <int PASSES, int EW, bool PAIR, int FMT = FMT_F16>
 __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_kernel(const __grid_constant__ GemmArgs args) {
   static_assert(EW == 8, "two epilogue warpgroups");
   using C = Cfg<PASSES, PAIR>;
+  constexpr int BKE = bk_elems<FMT>();   // k elements per k-block
   constexpr int PLANES = C::PLANES, STAGES = C::STAGES;
   // narrow GEMMs (N <= 64): N = 64 MMAs (half the tensor work of the padded 128-wide
   // tile); the pair's B halves become 32 rows each
-  const uint32_t IDESC = args.narrow ? ((Idesc<PAIR>::POS & ~(0x3Fu << 17)) | ((uint32_t)(64 >> 3) << 17))
-                                     : Idesc<PAIR>::POS;
+  const uint32_t IDESC = args.narrow ? ((Idesc<PAIR, FMT>::POS & ~(0x3Fu << 17)) | ((uint32_t)(64 >> 3) << 17))
+                                     : Idesc<PAIR, FMT>::POS;
   const uint32_t IDESC_NEG = IDESC | (1u << 13);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -260,7 +283,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int kblocks = (args.K + BK - 1) / BK;
+  const int kblocks = (args.K + BKE - 1) / BKE;
   const int kchunk = (args.kchunk > 0 && args.kchunk < kblocks) ? args.kchunk : kblocks;
   const int nchunks = (kblocks + kchunk - 1) / kchunk;
   // pair: CTA rank in the cluster; tiles are scheduled per pair
@@ -342,20 +365,20 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
 #pragma unroll
             for (int p = 0; p < PLANES; ++p)
-              tma_load_4d_pair(&args.mapA, st + p * PLANE_TILE, fb, kb * BK, arow, sa, p);
+              tma_load_4d_pair(&args.mapA, st + p * PLANE_TILE, fb, kb * BKE, arow, sa, p);
 #pragma unroll
             for (int p = 0; p < PLANES; ++p)
-              tma_load_4d_pair(&args.mapB2, st + PLANES * PLANE_TILE + p * C::B_TILE, fb, kb * BK,
+              tma_load_4d_pair(&args.mapB2, st + PLANES * PLANE_TILE + p * C::B_TILE, fb, kb * BKE,
                                brow, sb, p);
           } else {
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
 #pragma unroll
             for (int p = 0; p < PLANES; ++p)
-              tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BK, arow, sa, p);
+              tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BKE, arow, sa, p);
 #pragma unroll
             for (int p = 0; p < PLANES; ++p)
               tma_load_4d(&args.mapB, st + PLANES * PLANE_TILE + p * C::B_TILE, &full[stage],
-                          kb * BK, brow, sb, p);
+                          kb * BKE, brow, sb, p);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -391,8 +414,8 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
             // issued while the chunk accumulator is still ~2^-11 of its final size,
             // so the per-MMA RZ truncation only bites on the big·big MMAs.
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t koff = kk * 32;   // 16 fp16 = 32 B along K inside the swizzle row
+            for (int kk = 0; kk < 2; ++kk) {   // 2 x 32 B of K per 64-B row
+              const uint32_t koff = kk * 32;   // 16 fp16 / 8 tf32 = 32 B along K inside the swizzle row
               const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
               const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
               const uint64_t br = sdesc(sb0 + 0 * C::B_TILE + koff);
@@ -403,41 +426,41 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
               const uint64_t bil = sdesc(sb0 + 3 * C::B_TILE + koff);
               const uint32_t acc0 = (kin | kk) != 0;
               // real part: Ar·Br - Ai·Bi (cross terms)
-              mma_t<PAIR>(d_re, ar, brl, IDESC, acc0);
-              mma_t<PAIR>(d_re, arl, br, IDESC, 1);
-              mma_t<PAIR>(d_re, ail, bi, IDESC_NEG, 1);
-              mma_t<PAIR>(d_re, ai, bil, IDESC_NEG, 1);
+              mma_t<PAIR, FMT>(d_re, ar, brl, IDESC, acc0);
+              mma_t<PAIR, FMT>(d_re, arl, br, IDESC, 1);
+              mma_t<PAIR, FMT>(d_re, ail, bi, IDESC_NEG, 1);
+              mma_t<PAIR, FMT>(d_re, ai, bil, IDESC_NEG, 1);
               // imaginary part: Ar·Bi + Ai·Br (cross terms)
-              mma_t<PAIR>(d_im, ar, bil, IDESC, acc0);
-              mma_t<PAIR>(d_im, arl, bi, IDESC, 1);
-              mma_t<PAIR>(d_im, ai, brl, IDESC, 1);
-              mma_t<PAIR>(d_im, ail, br, IDESC, 1);
+              mma_t<PAIR, FMT>(d_im, ar, bil, IDESC, acc0);
+              mma_t<PAIR, FMT>(d_im, arl, bi, IDESC, 1);
+              mma_t<PAIR, FMT>(d_im, ai, brl, IDESC, 1);
+              mma_t<PAIR, FMT>(d_im, ail, br, IDESC, 1);
             }
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
+            for (int kk = 0; kk < 2; ++kk) {   // 2 x 32 B of K per 64-B row
               const uint32_t koff = kk * 32;
               const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
               const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
               const uint64_t br = sdesc(sb0 + 0 * C::B_TILE + koff);
               const uint64_t bi = sdesc(sb0 + 1 * C::B_TILE + koff);
-              mma_t<PAIR>(d_re, ar, br, IDESC, 1);        // big·big last
-              mma_t<PAIR>(d_re, ai, bi, IDESC_NEG, 1);
-              mma_t<PAIR>(d_im, ar, bi, IDESC, 1);
-              mma_t<PAIR>(d_im, ai, br, IDESC, 1);
+              mma_t<PAIR, FMT>(d_re, ar, br, IDESC, 1);        // big·big last
+              mma_t<PAIR, FMT>(d_re, ai, bi, IDESC_NEG, 1);
+              mma_t<PAIR, FMT>(d_im, ar, bi, IDESC, 1);
+              mma_t<PAIR, FMT>(d_im, ai, br, IDESC, 1);
             }
           } else {
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
+            for (int kk = 0; kk < 2; ++kk) {   // 2 x 32 B of K per 64-B row
               const uint32_t koff = kk * 32;
               const uint64_t ar = sdesc(st + 0 * PLANE_TILE + koff);
               const uint64_t ai = sdesc(st + 1 * PLANE_TILE + koff);
               const uint64_t br = sdesc(sb0 + 0 * C::B_TILE + koff);
               const uint64_t bi = sdesc(sb0 + 1 * C::B_TILE + koff);
               const uint32_t acc0 = (kin | kk) != 0;
-              mma_t<PAIR>(d_re, ar, br, IDESC, acc0);
-              mma_t<PAIR>(d_re, ai, bi, IDESC_NEG, 1);
-              mma_t<PAIR>(d_im, ar, bi, IDESC, acc0);
-              mma_t<PAIR>(d_im, ai, br, IDESC, 1);
+              mma_t<PAIR, FMT>(d_re, ar, br, IDESC, acc0);
+              mma_t<PAIR, FMT>(d_re, ai, bi, IDESC_NEG, 1);
+              mma_t<PAIR, FMT>(d_im, ar, bi, IDESC, acc0);
+              mma_t<PAIR, FMT>(d_im, ai, br, IDESC, 1);
             }
           }
           mma_commit_t<PAIR>(&empty[stage]);   // frees the smem stage(s) when these MMAs retire
@@ -764,10 +787,10 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
   }
 }
 
-template <int PASSES, int EW, bool PAIR>
+template <int PASSES, int EW, bool PAIR, int FMT = FMT_F16>
 cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
   const int smem = Cfg<PASSES, PAIR>::SMEM_BYTES + stage_bytes<EW>();
-  const void* kern = reinterpret_cast<const void*>(cgemm_tcgen05_kernel<PASSES, EW, PAIR>);
+  const void* kern = reinterpret_cast<const void*>(cgemm_tcgen05_kernel<PASSES, EW, PAIR, FMT>);
   if (cudaError_t e = set_smem_attr(kern, smem)) return e;
   if constexpr (PAIR) {
     // tiles of 256 rows, one per CTA pair (cluster of 2); persistent over the SMs
@@ -806,11 +829,11 @@ cudaError_t launch_impl(const GemmArgs& a, int num_sms, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, cgemm_tcgen05_kernel<PASSES, EW, PAIR>, p);
+    return cudaLaunchKernelEx(&cfg, cgemm_tcgen05_kernel<PASSES, EW, PAIR, FMT>, p);
   } else {
     int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
     if (grid < 1) grid = 1;
-    cgemm_tcgen05_kernel<PASSES, EW, PAIR><<<(unsigned)grid, 32 * EPI_WARP0 + 32 * EW, smem, s>>>(a);
+    cgemm_tcgen05_kernel<PASSES, EW, PAIR, FMT><<<(unsigned)grid, 32 * EPI_WARP0 + 32 * EW, smem, s>>>(a);
     return cudaGetLastError();
   }
 }
@@ -844,31 +867,41 @@ bool gemm_pair_ok(const GemmArgs& a, int min_m) {
   return min_m > 0 && a.M >= min_m && a.blk_slab_b == nullptr;
 }
 
-cudaError_t launch_gemm(const GemmArgs& a_in, int passes, int num_sms, cudaStream_t s) {
+cudaError_t launch_gemm(const GemmArgs& a_in, int passes, int num_sms, cudaStream_t s, int format) {
   GemmArgs a = a_in;
   a.narrow = (g_knobs.narrow_mma && a.N <= 64) ? 1 : 0;
   if (a.wave_sync) {
     cudaError_t e = cudaMemsetAsync(a.wave_ctr, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
   }
+  if (format == FMT_BF16)   // precision study formats (tn_cgemm): single-CTA tiles
+    return passes == 3 ? launch_impl<3, 8, false, FMT_BF16>(a, num_sms, s)
+                       : launch_impl<1, 8, false, FMT_BF16>(a, num_sms, s);
+  if (format == FMT_TF32)
+    return passes == 3 ? launch_impl<3, 8, false, FMT_TF32>(a, num_sms, s)
+                       : launch_impl<1, 8, false, FMT_TF32>(a, num_sms, s);
   if (a.use_pair)
     return passes == 3 ? launch_impl<3, 8, true>(a, num_sms, s) : launch_impl<1, 8, true>(a, num_sms, s);
   return passes == 3 ? launch_impl<3, 8, false>(a, num_sms, s) : launch_impl<1, 8, false>(a, num_sms, s);
 }
 
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
-                      int planes, int box_rows, char* err, size_t errcap) {
+                      int planes, int box_rows, char* err, size_t errcap, int format) {
+  const int esz = format == FMT_TF32 ? 4 : 2;
+  const CUtensorMapDataType dt = format == FMT_TF32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : format == FMT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                      : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     snprintf(err, errcap, "cuTensorMapEncodeTiled unavailable");
     return false;
   }
   cuuint64_t dims[4] = {(cuuint64_t)Kpad, (cuuint64_t)R, (cuuint64_t)G, (cuuint64_t)planes};
-  cuuint64_t strides[3] = {(cuuint64_t)(Kpad * 2), (cuuint64_t)(Kpad * 2 * R),
-                           (cuuint64_t)(Kpad * 2 * R * G)};
-  cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1, 1};
+  cuuint64_t strides[3] = {(cuuint64_t)(Kpad * esz), (cuuint64_t)(Kpad * esz * R),
+                           (cuuint64_t)(Kpad * esz * R * G)};
+  cuuint32_t box[4] = {(cuuint32_t)(64 / esz), (cuuint32_t)box_rows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides,
+  CUresult r = enc(map, dt, 4, const_cast<void*>(base), dims, strides,
                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {

@@ -9,6 +9,7 @@
 //                   sparse-merge gather tables (Eq. 7) and fused fp64 accumulate
 //   gather_out    — a9: merged-configuration order -> caller sample order
 #include "tn_internal.h"
+#include <cuda_bf16.h>
 
 #include <algorithm>
 
@@ -189,6 +190,54 @@ __global__ void __launch_bounds__(256, 4) prep_kernel(const PrepDesc* __restrict
             __floats2half2_rn(xr0 - fr.x, xr1 - fr.y);
         reinterpret_cast<__half2*>(d.dst + 3 * plane + idx)[0] =
             __floats2half2_rn(xi0 - fi.x, xi1 - fi.y);
+      }
+    }
+  }
+}
+
+// Operand prep for the precision-study formats of tn_cgemm (Fig. 4, Eq. 8):
+// a K-contiguous complex64 [G][R][K] operand -> planes re_big, im_big[, re_small,
+// im_small] of [G][R][Kpad] in bf16 (format 1) or tf32 in 32-bit containers (format 2),
+// big = rn(x·2^s), small = rn(x·2^s - big), both round-to-nearest-even (R11).
+__device__ __forceinline__ float rn_tf32(float x) {
+  uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;            // inf / nan
+  u += 0xfffu + ((u >> 13) & 1u);                            // RNE at bit 13
+  return __uint_as_float(u & 0xffffe000u);
+}
+
+__global__ void __launch_bounds__(256) prep_fmt_kernel(const float2* __restrict__ src, void* dst,
+                                                       int64_t rows, int64_t K, int64_t Kpad,
+                                                       int planes, int format,
+                                                       const unsigned* __restrict__ absmax,
+                                                       int* scale_out) {
+  const float amax = __uint_as_float(*absmax);
+  int s = 0;
+  if (amax > 0.f) {
+    int e;
+    frexpf(amax, &e);
+    s = max(-120, min(120, 15 - e));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scale_out = s;
+  const float sc = ldexpf(1.0f, s);
+  const int64_t plane = rows * Kpad;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < plane;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / Kpad, k = idx % Kpad;
+    const float2 v = k < K ? src[r * K + k] : make_float2(0.f, 0.f);
+    const float x[2] = {v.x * sc, v.y * sc};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (format == 2) {
+        float* P = reinterpret_cast<float*>(dst);
+        const float big = rn_tf32(x[c]);
+        P[c * plane + idx] = big;
+        if (planes == 4) P[(2 + c) * plane + idx] = rn_tf32(x[c] - big);
+      } else {
+        __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(dst);
+        const __nv_bfloat16 big = __float2bfloat16_rn(x[c]);
+        P[c * plane + idx] = big;
+        if (planes == 4) P[(2 + c) * plane + idx] = __float2bfloat16_rn(x[c] - __bfloat162float(big));
       }
     }
   }
@@ -1112,6 +1161,99 @@ __global__ void __launch_bounds__(256) einsum_wdot_kernel(const EinsumDesc* __re
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// Variant for batched merges whose per-batch output is tiny (M <= 4 rows, N <= 32; e.g.
+// the final merge of a sparse-state path: J = 65 536 batches of 4 x 16 outputs, K = 2048):
+// a warp computes all M rows x NN = 8 columns of one batch j (ceil(N/8) warps per batch),
+// so each k of the B slab is read once per batch instead of once per output row and each
+// A row is reused for 8 columns; lanes stride K, two k per lane per iteration with all
+// loads issued before the FMAs; fp32 lane sums, fp64 warp reduction.
+template <int MM, int NN>
+__global__ void __launch_bounds__(128) einsum_wdotj_kernel(const EinsumDesc* __restrict__ gd,
+                                                           const int64_t* __restrict__ leaf_off) {
+  static_assert(MM * NN <= 32, "at most 32 outputs per warp (1 per lane)");
+  __shared__ __align__(16) EinsumDesc d;
+  copy_desc_to_smem(&d, gd);
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = (int)d.M, N = (int)d.N;
+  const int NH = (N + NN - 1) / NN;     // warps per batch
+  float amax = 0.f;
+  __shared__ int64_t am[MM], bn[32];    // row offsets (same for every batch)
+  if (threadIdx.x < MM) am[threadIdx.x] = threadIdx.x < M ? decompose(threadIdx.x, d.nm, d.m_ext, d.m_sa) : 0;
+  if (threadIdx.x < 32) bn[threadIdx.x] = threadIdx.x < N ? decompose(threadIdx.x, d.nn, d.n_ext, d.n_sb) : 0;
+  __syncthreads();
+  auto koffs = [&](int64_t k, int64_t& ka, int64_t& kb) {
+    int64_t t = k;
+    ka = 0;
+    kb = 0;
+    for (int i = d.nk - 1; i >= 0; --i) {
+      const int sh = d.k_sh[i];
+      const int64_t dg = d.pow2 ? (t & ((int64_t(1) << sh) - 1)) : t % d.k_ext[i];
+      t = d.pow2 ? (t >> sh) : t / d.k_ext[i];
+      ka += dg * d.k_sa[i];
+      kb += dg * d.k_sb[i];
+    }
+  };
+  const int64_t units = d.J * NH;
+  for (int64_t u_ = blockIdx.x * 4 + warp; u_ < units; u_ += (int64_t)gridDim.x * 4) {
+    const int64_t j = u_ / NH;
+    const int n0 = (int)(u_ % NH) * NN;
+    const int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs;
+    const int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs;
+    float cr[MM][NN], ci[MM][NN];
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+#pragma unroll
+      for (int n = 0; n < NN; ++n) { cr[m][n] = 0.f; ci[m][n] = 0.f; }
+    for (int64_t k0 = lane; k0 < d.K; k0 += 64) {
+      const bool two = k0 + 32 < d.K;
+      int64_t ka0, kb0, ka1 = 0, kb1 = 0;
+      koffs(k0, ka0, kb0);
+      if (two) koffs(k0 + 32, ka1, kb1);
+      float2 a[2][MM], b[2][NN];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const bool ok = u == 0 || two;
+        const int64_t ka = u ? ka1 : ka0, kb = u ? kb1 : kb0;
+#pragma unroll
+        for (int m = 0; m < MM; ++m)
+          a[u][m] = (ok && m < M) ? __ldg(A + ao + am[m] + ka) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+          b[u][n] = (ok && n0 + n < N) ? __ldg(B + bo + bn[n0 + n] + kb) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int m = 0; m < MM; ++m) {
+            cr[m][n] = fmaf(a[u][m].x, b[u][n].x, fmaf(-a[u][m].y, b[u][n].y, cr[m][n]));
+            ci[m][n] = fmaf(a[u][m].x, b[u][n].y, fmaf(a[u][m].y, b[u][n].x, ci[m][n]));
+          }
+    }
+    // output (m, n0 + n) is reduced onto lane m * NN + n
+    double orr = 0.0, oi = 0.0;
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+#pragma unroll
+      for (int n = 0; n < NN; ++n) {
+        if (m < M && n0 + n < N) {
+          double r = cr[m][n], i = ci[m][n];
+          for (int o = 16; o > 0; o >>= 1) {
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+            i += __shfl_xor_sync(0xffffffffu, i, o);
+          }
+          if (lane == m * NN + n) { orr = r; oi = i; }
+        }
+      }
+    const int m = lane / NN, n = n0 + lane % NN;
+    if (m < M && n < N && lane < MM * NN) store_out(d, (j * M + m) * N + n, orr, oi, amax);
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
 // Variant for operands whose unit stride is the output dim n: lane = (k group, n), so
 // each load instruction reads NL consecutive n of 32/NL k values; one fp32 partial per
 // lane, reduced across the k groups in fp64.
@@ -1235,6 +1377,16 @@ int grid_for(int64_t total, int threads) {
 }
 
 }  // namespace
+
+cudaError_t launch_prep_fmt(const float2* src, void* dst, int64_t rows, int64_t K, int64_t Kpad,
+                            int planes, int format, const unsigned* absmax, int* scale_out,
+                            cudaStream_t s) {
+  const int64_t n = rows * Kpad;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  prep_fmt_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(src, dst, rows, K, Kpad, planes,
+                                                                       format, absmax, scale_out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_set_counter(int64_t* counter, int64_t value, cudaStream_t s) {
   set_counter_kernel<<<1, 1, 0, s>>>(counter, value);
@@ -1410,7 +1562,8 @@ int einsum_variants(const EinsumDesc& h) {
   if (h.mode == 1) return h.J > 1 ? 1 : 4;   // 0 heuristic rows, 1 previous design, 2..3: R = 1, 2
                                              // (batched merges: the new design only)
   if (h.mode == 3) return 2;   // 0 new design, 1 previous design
-  if (h.mode == 4) return 2;   // 0 lanes over k, 1 lanes over (k group, n)
+  if (h.mode == 4)             // 0 lanes over k, 1 lanes over (k group, n), 2 warps per batch
+    return h.M <= 4 ? 3 : 2;
   return 1;
 }
 
@@ -1492,7 +1645,11 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     const int64_t rows = h.J * h.M;
     int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    if (variant == 1)
+    if (variant == 2) {
+      int64_t jb = (h.J * ((h.N + 7) / 8) + 3) / 4;
+      if (jb > 148 * 24) jb = 148 * 24;
+      einsum_wdotj_kernel<4, 8><<<(unsigned)std::max<int64_t>(jb, 1), 128, 0, s>>>(d_desc, leaf_off);
+    } else if (variant == 1)
       einsum_wdot2_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(d_desc, leaf_off);
     else
       einsum_wdot_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(d_desc, leaf_off);

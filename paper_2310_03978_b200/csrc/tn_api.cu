@@ -526,6 +526,11 @@ bool plan_gate(tn::PrepDesc& p, const tn::EinsumDesc& e, std::vector<int64_t>& t
   for (int b = 0; b < nb; ++b) if (nbit[b] >= 0) { in[b] = 1; ++td; }
   if (ts_of(td) > 12 || td > 12) return false;
   for (int b = 0; b < 3; ++b) add(b);
+  // an expanding gate (N >= K) writes at least as many bytes as it reads: destination
+  // bits 3-4 next, so a tile's plane stores are 64-B runs (whole sectors) instead of
+  // scattered 16-B vectors (C4-sparse step 210 -> 217: N = 16, K = 4)
+  if (e.N >= e.K)
+    for (int b = 3; b < 5 && b < nb; ++b) add(b);
   std::vector<int> bysrc;                          // carry bits by X weight
   for (int b = 0; b < nb; ++b) if (nbit[b] < 0) bysrc.push_back(b);
   std::stable_sort(bysrc.begin(), bysrc.end(), [&](int a, int b) { return xw[a] < xw[b]; });
@@ -2015,7 +2020,9 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
         }
         for (int v = 0; v < 2 * nv; ++v) cudaEventDestroy(ev[v]);
       }
-      int var = sp.simt_variant < 0 ? 0 : sp.simt_variant;
+      // untuned (accumulating final steps are never re-run): batched merges with a tiny
+      // per-batch output take the warp-per-batch kernel
+      int var = sp.simt_variant >= 0 ? sp.simt_variant : (sp.hdesc.mode == 4 && nv == 3 ? 2 : 0);
       if (c->simt_force >= 0) var = std::min(c->simt_force, nv - 1);
       Timer tm(c, 2, sp.tcc, sp.tmc, (int)s, sm);
       TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, var));
@@ -2620,11 +2627,12 @@ tn_status tn_reset_kernel_stats(tn_ctx* c) {
 
 tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t J, int64_t m, int64_t n,
                    int64_t k, int64_t ga, int64_t gb, const int32_t* ia, const int32_t* ib, int passes,
-                   int force_simt) {
+                   int force_simt, int format) {
   if (!c) return fail(TN_ERR_USAGE, "null context");
   if (c->host_only) return fail(TN_ERR_USAGE, "host-only context (device -1) cannot execute");
   if (J < 1 || m < 1 || n < 1 || k < 1 || ga < 1 || gb < 1) return fail(TN_ERR_USAGE, "bad sizes");
   if (passes != 1 && passes != 3) return fail(TN_ERR_USAGE, "passes must be 1 or 3");
+  if (format < 0 || format > 2) return fail(TN_ERR_USAGE, "format must be 0 (fp16), 1 (bf16) or 2 (tf32)");
   TN_CUDA(cudaSetDevice(c->device));
   cudaStream_t sm = c->stream;
   unsigned* am = nullptr;
@@ -2657,8 +2665,9 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     mem_free(c, d);
   } else {
     const int64_t Kpad = (k + 7) / 8 * 8;
-    const int64_t b0 = (4 * ga * m * Kpad * 2 + 1023) / 1024 * 1024;
-    const int64_t b1 = (4 * gb * n * Kpad * 2 + 1023) / 1024 * 1024;
+    const int64_t esz = format == 2 ? 4 : 2;
+    const int64_t b0 = (4 * ga * m * Kpad * esz + 1023) / 1024 * 1024;
+    const int64_t b1 = (4 * gb * n * Kpad * esz + 1023) / 1024 * 1024;
     uint8_t* scr = nullptr;
     if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&scr), b0 + b1)) return st1;
     tn::PrepDesc p[2];
@@ -2679,8 +2688,10 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
       p[side].plane_elems = G * R * Kpad;
       p[side].absmax_in = am + side;
       p[side].scale_out = sc + side;
-      if (!tn::encode_plane_map(side ? &g.mapB : &g.mapA, p[side].dst, Kpad, R, G, 4, 128, err, sizeof(err)) ||
-          (side == 1 && !tn::encode_plane_map(&g.mapB2, p[side].dst, Kpad, R, G, 4, 64, err, sizeof(err)))) {
+      if (!tn::encode_plane_map(side ? &g.mapB : &g.mapA, p[side].dst, Kpad, R, G, 4, 128, err, sizeof(err),
+                                format) ||
+          (side == 1 && !tn::encode_plane_map(&g.mapB2, p[side].dst, Kpad, R, G, 4, 64, err, sizeof(err),
+                                              format))) {
         mem_free(c, scr);
         return fail(TN_ERR_INTERNAL, err);
       }
@@ -2689,8 +2700,13 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&dp), sizeof(p))) return st1;
     TN_CUDA(cudaMemcpyAsync(dp, p, sizeof(p), cudaMemcpyHostToDevice, sm));
     const int planes = passes == 3 ? 4 : 2;
-    TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, 0, 0, nullptr, sm));
-    TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, 0, 0, nullptr, sm));
+    if (format == 0) {
+      TN_CUDA(tn::launch_prep(dp, p[0].plane_elems, planes, 0, 0, nullptr, sm));
+      TN_CUDA(tn::launch_prep(dp + 1, p[1].plane_elems, planes, 0, 0, nullptr, sm));
+    } else {
+      TN_CUDA(tn::launch_prep_fmt(A2, p[0].dst, ga * m, k, Kpad, planes, format, am, sc, sm));
+      TN_CUDA(tn::launch_prep_fmt(B2, p[1].dst, gb * n, k, Kpad, planes, format, am + 1, sc + 1, sm));
+    }
     g.J = (int32_t)J; g.M = (int32_t)m; g.N = (int32_t)n; g.K = (int32_t)k;
     g.ia = ia; g.ib = ib;
     g.C = reinterpret_cast<float2*>(C);
@@ -2701,14 +2717,14 @@ tn_status tn_cgemm(tn_ctx* c, const float* A, const float* B, float* C, int64_t 
     g.n_tiles = (int64_t)g.tiles_m * g.tiles_n * J;
     g.kchunk = passes == 3 ? c->kchunk3 : c->kchunk1;
     g.group_m = c->group_m;
-    g.use_pair = tn::gemm_pair_ok(g, tn::g_knobs.pair_min_m) ? 1 : 0;
+    g.use_pair = (format == 0 && tn::gemm_pair_ok(g, tn::g_knobs.pair_min_m)) ? 1 : 0;
     if (!c->d_wave)
       if (tn_status st1 = mem_alloc(c, reinterpret_cast<void**>(&c->d_wave), sizeof(unsigned long long))) return st1;
     g.wave_ctr = c->d_wave;
     g.wave_sync = (env_int("TN_WAVE_SYNC", 1) && k >= 1024) ? 1 : 0;
     {
       Timer tm(c, 0, 8.0 * (double)J * m * n * k, 8.0 * (double)(ga * m * k + gb * n * k + J * m * n));
-      TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm));
+      TN_CUDA(tn::launch_gemm(g, passes, c->num_sms, sm, format));
     }
     cudaError_t e = cudaStreamSynchronize(sm);
     mem_free(c, dp);

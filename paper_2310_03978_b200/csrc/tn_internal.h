@@ -189,11 +189,16 @@ int einsum_variants(const EinsumDesc& host_desc);
 cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
                               const int* flag, cudaStream_t s);
 cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);
-cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s);
+// precision-study operand prep (bf16 = 1 / tf32 = 2 planes) of a K-contiguous [rows][K] operand
+cudaError_t launch_prep_fmt(const float2* src, void* dst, int64_t rows, int64_t K, int64_t Kpad,
+                            int planes, int format, const unsigned* absmax, int* scale_out,
+                            cudaStream_t s);
+// format: 0 = fp16 planes (product path), 1 = bf16, 2 = tf32 (precision study, tn_cgemm)
+cudaError_t launch_gemm(const GemmArgs& a, int passes, int num_sms, cudaStream_t s, int format = 0);
 // CTA-pair eligibility: M >= min_m (g_knobs.pair_min_m, default 512; 0 = never) and
 // one B slab per 256-row tile (not a grouped merge)
 bool gemm_pair_ok(const GemmArgs& a, int min_m);
 bool encode_plane_map(CUtensorMap* map, const void* base, int64_t Kpad, int64_t R, int64_t G,
-                      int planes, int box_rows, char* err, size_t errcap);
+                      int planes, int box_rows, char* err, size_t errcap, int format = 0);
 
 }  // namespace tn

@@ -119,7 +119,7 @@ def lib():
         "tn_get_kernel_stats": [VP, C.c_int, P(KernelStats)],
         "tn_reset_kernel_stats": [VP],
         "tn_get_step_stats": [VP, C.c_int, I64, VP],
-        "tn_cgemm": [VP, VP, VP, VP, I64, I64, I64, I64, I64, I64, VP, VP, C.c_int, C.c_int],
+        "tn_cgemm": [VP, VP, VP, VP, I64, I64, I64, I64, I64, I64, VP, VP, C.c_int, C.c_int, C.c_int],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -296,9 +296,12 @@ class Contraction:
         self.set_path(path)
         return self.set_slices(sliced)
 
+    FORMATS = {"fp16": 0, "bf16": 1, "tf32": 2}
+
     def cgemm(self, A, B, Cout, J, m, n, k, ga=1, gb=1, ia=None, ib=None, passes=3,
-              force_simt=False):
-        """Stand-alone complex GEMM on torch complex64 CUDA tensors (unit tests)."""
+              force_simt=False, fmt="fp16"):
+        """Stand-alone complex GEMM on torch complex64 CUDA tensors (unit tests, the
+        precision study); fmt = operand format of the tensor-core path (tn_cgemm)."""
         _check(lib().tn_cgemm(self._h, _tptr(A), _tptr(B), _tptr(Cout), int(J), int(m), int(n),
                               int(k), int(ga), int(gb), _tptr(ia), _tptr(ib), int(passes),
-                              int(bool(force_simt))))
+                              int(bool(force_simt)), self.FORMATS[fmt]))

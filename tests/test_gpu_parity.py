@@ -134,6 +134,7 @@ ROUTES = {
     "simt_wide": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SKINNY_MAX_SMALL": "0"},
     "simt_wdot": {"TN_DISABLE_TC": "1", "TN_WDOT_MIN_K": "2"},
     "simt_wdot2": {"TN_DISABLE_TC": "1", "TN_WDOT_MIN_K": "2", "TN_SIMT_VARIANT": "1"},
+    "simt_wdotj": {"TN_DISABLE_TC": "1", "TN_WDOT_MIN_K": "2", "TN_SIMT_VARIANT": "2"},
     "simt_variant1": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "1"},
     "simt_variant2": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "2"},
     "simt_variant3": {"TN_DISABLE_TC": "1", "TN_SKINNY_MIN_BIG": "2", "TN_SIMT_VARIANT": "3"},

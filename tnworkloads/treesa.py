@@ -95,7 +95,9 @@ class Tree:
             ln += ub
         out = (La ^ Lb).bit_count() + self.log2U(Qa | Qb)
         cost = 2.0 ** (lj + lm + ln + lk + 3.0)
-        if self.beta:
+        if self.beta and min(lm, ln) >= 4.0 and lk >= 4.0 and max(lm, ln) >= 7.0:
+            # only GEMM-shaped steps (the executor's tensor-core routing thresholds): small
+            # gate absorptions are HBM-bound either way and carry alpha's T_mc term
             lu = min(0.0, lk - 6.0) + min(0.0, min(lm, ln) - 5.0)   # log2 u
             if lu < 0.0:
                 cost += self.beta * cost * (2.0 ** -lu - 1.0)

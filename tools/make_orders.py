@@ -35,9 +35,13 @@ def main():
     for s in range(args.seeds):
         t = time.time()
         p0 = bisection_path(w.net, w.samples, seed=3004 + s, leaf_size=8, time_weight=0.3)
-        path, sliced, tot, pk = optimize(w.net, w.samples, p0, args.peak, seed=3004 + s,
-                                         sweeps=args.sweeps, alpha=args.alpha,
-                                         beta=args.beta)
+        try:
+            path, sliced, tot, pk = optimize(w.net, w.samples, p0, args.peak, seed=3004 + s,
+                                             sweeps=args.sweeps, alpha=args.alpha,
+                                             beta=args.beta)
+        except RuntimeError as e:      # e.g. the slice limit: try the next seed
+            print(f"seed {s}: {e}", flush=True)
+            continue
         pc = path_cost(w.net, w.samples, path, sliced)
         score = tot * 2.0 ** len(sliced)
         print(f"seed {s}: per-slice {pc.flops_per_slice:.3g} peak 2^{pc.peak_log2:.1f} "

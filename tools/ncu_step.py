@@ -34,9 +34,12 @@ def main():
     steps = ctx.plan_json()["steps"]
     if a.step >= 0:
         gemm_before = sum(1 for s in steps[:a.step] if s["route"] == "tcgen05")
+        gate_before = sum(p.count(5) for s in steps[:a.step] if s["route"] == "tcgen05"
+                          for p in [s["prep"]])
         print(f"step {a.step}: {steps[a.step]['route']} J={steps[a.step]['J']} m={steps[a.step]['m']} "
-              f"n={steps[a.step]['n']} k={steps[a.step]['k']}; cgemm launches before it in a slice: "
-              f"{gemm_before}", flush=True)
+              f"n={steps[a.step]['n']} k={steps[a.step]['k']} prep={steps[a.step]['prep']}; in a slice, "
+              f"cgemm launches before it: {gemm_before}, prep_gate launches before it: {gate_before}",
+              flush=True)
     ctx.contract(0, 3, a.precision)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()

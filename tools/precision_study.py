@@ -1,10 +1,13 @@
 """Precision micro-study (the Fig. 4 analogue):
-complex dot products (as 128 x 128 x K GEMMs on the tensor cores) of data with
-magnitudes 1e-7 .. 1e3, relative error vs an fp64 product for
-  - 3xFP16 with power-of-two rescaling (this library's extended mode),
-  - 1xFP16 with rescaling (mixed mode),
-  - fp32 SIMT (this library's CUDA-core path, fp64 accumulation),
-  - fp32 matmul with fp32 accumulation (numpy float32, the paper's FP32 baseline).
+complex dot products (as 128 x 128 x K GEMMs) of data with magnitudes 1e-7 .. 1e3
+(one row per magnitude, plus a row whose entries are log-uniform over the whole
+"FP16 range"), relative error vs the fp64 product of the same fp32 inputs, for the
+Fig. 4 set on B200:
+  - FP32: CUDA-core fp32 GEMM (torch.matmul, TF32 off) and numpy float32,
+  - 1xTF32 / 3xTF32 (Eq. 8 as printed; tcgen05 kind::tf32, RN split),
+  - 1xBF16 / 3xBF16 (kind::f16 with bf16 operands, RN split),
+  - 1xFP16 / 3xFP16 with power-of-two rescaling (this library's mixed / extended mode),
+  - the library's SIMT path (fp32 products, fp64 sums).
 
     python tools/precision_study.py [--k 16384] [--out file.json]"""
 import argparse
@@ -18,9 +21,49 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2310_03978_b200 import Contraction  # noqa: E402
 
+SCHEMES = [("1xtf32", 1, "tf32"), ("3xtf32", 3, "tf32"), ("1xbf16", 1, "bf16"),
+           ("3xbf16", 3, "bf16"), ("1xfp16", 1, "fp16"), ("3xfp16", 3, "fp16")]
+
 
 def rel(x, ref):
     return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
+def operands(rng, m, n, k, magnitude):
+    """Complex normal data at one magnitude, or (magnitude None) entries whose moduli
+    are log-uniform over [1e-7, 1e3] with uniform phases."""
+    def one(r):
+        if magnitude is None:
+            mod = 10.0 ** rng.uniform(-7, 3, (r, k))
+            return mod * np.exp(2j * np.pi * rng.random((r, k)))
+        return (rng.standard_normal((r, k)) + 1j * rng.standard_normal((r, k))) * magnitude
+    return one(m).astype(np.complex64), one(n).astype(np.complex64)
+
+
+def study(ctx, k=16384, m=128, n=128, magnitudes=tuple(10.0 ** e for e in range(-7, 4)) + (None,),
+          seed=5):
+    rng = np.random.default_rng(seed)
+    rows = []
+    for mag in magnitudes:
+        A32, B32 = operands(rng, m, n, k, mag)
+        ref = A32.astype(np.complex128) @ B32.astype(np.complex128).T     # exact on the fp32 inputs
+        tA = torch.from_numpy(A32).cuda().reshape(1, m, k)
+        tB = torch.from_numpy(B32).cuda().reshape(1, n, k)
+        res = {"magnitude": "log-uniform 1e-7..1e3" if mag is None else mag}
+        for tag, passes, fmt in SCHEMES:
+            tC = torch.empty(1, m, n, dtype=torch.complex64, device="cuda")
+            ctx.cgemm(tA, tB, tC, 1, m, n, k, passes=passes, fmt=fmt)
+            res[tag] = rel(tC[0].cpu().numpy().astype(np.complex128), ref)
+        tC = torch.empty(1, m, n, dtype=torch.complex64, device="cuda")
+        ctx.cgemm(tA, tB, tC, 1, m, n, k, force_simt=True)
+        res["simt"] = rel(tC[0].cpu().numpy().astype(np.complex128), ref)
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        res["fp32_cuda_core"] = rel((tA[0] @ tB[0].T).cpu().numpy().astype(np.complex128), ref)
+        torch.backends.cuda.matmul.allow_tf32 = prev
+        res["fp32_numpy"] = rel((A32 @ B32.T).astype(np.complex128), ref)
+        rows.append(res)
+    return rows
 
 
 def main():
@@ -28,29 +71,13 @@ def main():
     ap.add_argument("--k", type=int, default=16384)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    m = n = 128
     ctx = Contraction(0, torch.cuda.current_stream())
-    rng = np.random.default_rng(5)
-    rows = []
-    for e in range(-7, 4):
-        scale = 10.0 ** e
-        A = (rng.standard_normal((m, a.k)) + 1j * rng.standard_normal((m, a.k))) * scale
-        B = (rng.standard_normal((n, a.k)) + 1j * rng.standard_normal((n, a.k))) * scale
-        A32, B32 = A.astype(np.complex64), B.astype(np.complex64)
-        ref = A32.astype(np.complex128) @ B32.astype(np.complex128).T     # exact on the fp32 inputs
-        res = {"magnitude": scale}
-        for tag, passes, simt in (("3xfp16", 3, False), ("1xfp16", 1, False), ("fp32_simt", 3, True)):
-            tA = torch.from_numpy(A32).cuda().reshape(1, m, a.k)
-            tB = torch.from_numpy(B32).cuda().reshape(1, n, a.k)
-            tC = torch.empty(1, m, n, dtype=torch.complex64, device="cuda")
-            ctx.cgemm(tA, tB, tC, 1, m, n, a.k, passes=passes, force_simt=simt)
-            res[tag] = rel(tC[0].cpu().numpy().astype(np.complex128), ref)
-        res["fp32_numpy"] = rel((A32 @ B32.T).astype(np.complex128), ref)
-        rows.append(res)
-        print(json.dumps(res))
+    rows = study(ctx, a.k)
+    for r in rows:
+        print(json.dumps(r))
     ctx.close()
     if a.out:
-        json.dump({"k": a.k, "rows": rows}, open(a.out, "w"), indent=1)
+        json.dump({"k": a.k, "m": 128, "n": 128, "rows": rows}, open(a.out, "w"), indent=1)
 
 
 if __name__ == "__main__":
