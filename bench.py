@@ -40,7 +40,7 @@ def parse(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c4", "c3", "c2"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5", "c3", "c2"])
     # headline: the paper's sampling boundary (2^16 uniform samples) with
     # per-slice intermediates up to 2^32 elements (32 GiB: sized for 180 GB of HBM3e;
     # DESIGN.md §3 "Why peak 2^32"); --boundary single is the secondary line
@@ -63,6 +63,9 @@ def load_workload(args):
         return configs.c2()
     if args.workload == "c3":
         return configs.c3()
+    if args.workload == "c5":
+        return configs.c5("single" if args.boundary == "sparse16" else args.boundary, args.peak,
+                          args.order_tag)
     return configs.c4(args.boundary, args.peak, args.order_tag)
 
 

@@ -80,7 +80,7 @@ struct Cfg {
 // per-warp staging tile for plane outputs whose unit-stride dim is a row dim
 // (8 epilogue warps only: 16 would exceed the 227 KB shared-memory limit)
 template <int EW>
-constexpr int stage_bytes() { return EW == 8 ? EW * 32 * 9 * 8 : 0; }
+constexpr int stage_bytes() { return EW == 8 ? EW * 32 * 10 * 8 : 0; }
 
 // instruction descriptor: D=f32 (bits 4-5 = 1), A/B format at bits 7-9 / 10-12 (kind::f16:
 // 0 = f16, 1 = bf16; kind::tf32: 2 = tf32), K-major, N>>3 at bits 17-22, M>>4 at bits
@@ -233,6 +233,38 @@ __device__ __forceinline__ void fence_after() {
 
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Row-contiguous output through a per-warp smem stage.  The TMEM layout gives each
+// lane one row, so a direct store instruction touches 32 rows with 16 B each (32
+// half-filled sectors: the LSU, not DRAM, bounds output-heavy GEMMs).  Here the warp
+// writes 8 columns of its 32 rows into smem (row stride 10 float2: 16-B aligned,
+// conflict-free), then each store instruction writes 8 rows x 64 contiguous bytes.
+// base = element offset of this lane's row start (column n0); valid = the row exists.
+template <int WC>
+__device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, const float* si,
+                                                  float2* C, int64_t base, bool valid, int lane,
+                                                  float& amax) {
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int i = 0; i < WC; i += 8) {
+    float4* w = reinterpret_cast<float4*>(buf + lane * 10);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float r0 = sr[i + 2 * c], i0 = si[i + 2 * c], r1 = sr[i + 2 * c + 1], i1 = si[i + 2 * c + 1];
+      w[c] = make_float4(r0, i0, r1, i1);
+      if (valid) amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = (lane >> 2) + 8 * q, c = lane & 3;
+      const int64_t rb = __shfl_sync(0xffffffffu, base, r);
+      const float4 v = reinterpret_cast<const float4*>(buf + r * 10)[c];
+      if ((vmask >> r) & 1u) *reinterpret_cast<float4*>(C + rb + i + 2 * c) = v;
+    }
+    __syncwarp();
+  }
 }
 
 // Tile index -> (j, mt, nt).  Tiles of one batch are visited in groups of
@@ -504,6 +536,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
     const uint32_t ce0 = PAIR ? map_rank(&cempty[0], 0) : 0;   // leader's drain barriers
     const uint32_t ce1 = PAIR ? map_rank(&cempty[1], 0) : 0;
     int titer = 0;
+    int tab_nt = -1, tab_sel = 0;           // out_gen column table: tile column it holds
     for (int64_t tile = unit; tile < args.n_tiles; tile += units, ++titer) {
       int j, mt, nt;
       decode_tile(args, tile, j, mt, nt);
@@ -545,10 +578,13 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       int m = mt * C::TILE_M + (int)rank * BM + row;
       const int n0 = nt * BN + half * WC;
       if (args.out_gen) {
-        // ---- general output map: column offsets of this tile into smem, then stores
-        int64_t* tab = noff_tab + (titer & 1) * BN;
+        // ---- general output map: column offsets of this tile into smem (recomputed only
+        // when the tile column changes; double-buffered), then stores
+        const bool new_nt = nt != tab_nt;
+        if (new_nt) { tab_nt = nt; ++tab_sel; }
+        int64_t* tab = noff_tab + (tab_sel & 1) * BN;
         const int et = threadIdx.x - 32 * EPI_WARP0;     // epilogue thread 0 .. 32*EW-1
-        if (et < BN) {
+        if (new_nt && et < BN) {
           int64_t t = (int64_t)nt * BN + et, off = 0;
           for (int q = args.n_qo - 1; q >= 0; --q) {
             const int sh = args.qo_sh[q];
@@ -557,7 +593,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
           }
           tab[et] = off;
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
+        if (new_nt) asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
         if (args.out_planes) {
           // ---- fused consumer prep: 8 destination-contiguous columns -> one 16-B vector
           // per fp16 plane (RN hi, RN lo = rn(x - hi), Eq. 8), scaled by 2^plane_exp
@@ -578,7 +614,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
               // unit-stride plane dim = the 8 lowest row bits: stage 8 columns of the
               // warp's 32 rows in smem, then lane (group g, column c) writes rows
               // 8g..8g+7 of column c as one 16-B vector per plane
-              float2* buf = stage_buf + (warp - EPI_WARP0) * 32 * 9;
+              float2* buf = stage_buf + (warp - EPI_WARP0) * 32 * 10;
               const int g = lane >> 3, cc = lane & 7;
               const int64_t gb = __shfl_sync(0xffffffffu, rb, 8 * g);
 #pragma unroll
@@ -638,6 +674,19 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
           }
           continue;
         }
+        if (EW == 8 && args.cols_contig && n0 + WC <= args.N) {
+          // the 64 columns of every row are one contiguous, 16-B aligned output run
+          int64_t t = m < args.M ? m : 0, moff = 0;
+          for (int q = args.n_po - 1; q >= 0; --q) {
+            const int sh = args.po_sh[q];
+            moff += (t & ((int64_t(1) << sh) - 1)) * args.po_str[q];
+            t >>= sh;
+          }
+          const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff + tab[half * WC];
+          store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C, rb, m < args.M,
+                                lane, amax);
+          continue;
+        }
         if (m < args.M && n0 < args.N) {
           int64_t t = m, moff = 0;
           for (int q = args.n_po - 1; q >= 0; --q) {
@@ -647,17 +696,6 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
           }
           const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff;
           const int64_t* tc = tab + half * WC;
-          if (args.cols_contig && n0 + WC <= args.N) {
-            // the 64 columns are one contiguous, 16-B aligned output run
-            float4* dst = reinterpret_cast<float4*>(args.C + rb + tc[0]);
-#pragma unroll
-            for (int i = 0; i < WC / 2; ++i) {
-              const float r0 = sr[2 * i], i0 = si[2 * i], r1 = sr[2 * i + 1], i1 = si[2 * i + 1];
-              dst[i] = make_float4(r0, i0, r1, i1);
-              amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
-            }
-            continue;
-          }
           if (args.cols_stride > 1) {
             // one strided column dim (the consumer's unit-stride dim is a row dim): a
             // column's offset is n * stride, no table reads or contiguity tests
@@ -731,6 +769,11 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       }
       int64_t orow = (int64_t)j * args.M + m;
       if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
+      if (EW == 8 && !args.acc && (args.N % 2) == 0 && n0 + WC <= args.N) {
+        store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C,
+                              orow * (int64_t)args.N + n0, m < args.M && orow >= 0, lane, amax);
+        continue;
+      }
       if (m < args.M && n0 < args.N && orow >= 0) {
         const int64_t base = orow * (int64_t)args.N + n0;
         if (args.acc) {

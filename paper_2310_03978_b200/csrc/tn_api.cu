@@ -882,6 +882,8 @@ tn_status build_plan(tn_ctx* c) {
   const int dot_min_k = env_int("TN_DOT_MIN_K", 4096);
   const int dot_max_out = env_int("TN_DOT_MAX_OUT", 4096);
   const int tc_deep_k = env_int("TN_TC_DEEP_K", 1024);
+  const int64_t tc_out_min = env_int("TN_TC_OUT_MIN", 1 << 20);   // 0: never (see below)
+  const int tc_out_side = env_int("TN_TC_OUT_SIDE", 32);
   const int wdot_min_k = env_int("TN_WDOT_MIN_K", 256);    // SIMT mode 4 (warp dot) from this K
   const int skinny_max_small = env_int("TN_SKINNY_MAX_SMALL", 64);
   const int prep_force = env_int("TN_PREP_FORCE", -1);   // tests: force a prep kernel kind
@@ -1169,6 +1171,17 @@ tn_status build_plan(tn_ctx* c) {
           sp.x_is_b = true;
         }
       }
+    }
+    // A step left to the general SIMT kernel (mode 0: one thread per output with a full
+    // index decomposition) whose output is large and whose free sides are both GEMM-sized
+    // -- e.g. a batched merge with a tiny K (C4-sparse: J = 32 batches of 4096 x 2048,
+    // K = 4) -- runs on the tensor cores instead: the GEMM streams its output from TMEM
+    // (K is zero-padded to one k-block; the MMA work is negligible next to the stores).
+    if (!sp.tc && sp.mode == 0 && !disable_tc && !sp.final_step && tc_out_min > 0 &&
+        sp.J * sp.m * sp.n >= tc_out_min && std::min(sp.m, sp.n) >= tc_out_side && std::max(sp.m, sp.n) >= tc_big &&
+        sp.m < INT32_MAX && sp.n < INT32_MAX && sp.J < INT32_MAX) {
+      sp.tc = true;
+      sp.swap = sp.n > sp.m;
     }
     std::vector<VDim> od;
     const auto& kc = consumer_k[s];

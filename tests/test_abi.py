@@ -96,6 +96,14 @@ def test_c2_plan_matches_oracle_bookkeeping():
     assert c.info()["n_out"] == 1024
 
 
+def test_c5_m20_plan_matches_oracle_bookkeeping():
+    """C5 (m=20, 430 fsim tensors): the cached order's plan at full size, bit-exact."""
+    w = configs.c5()
+    c, pj = _check_plan(w)
+    assert len(pj["steps"]) == len(w.net.labels) - 1
+    assert pj["peak_elements"] <= 2.0 ** 32
+
+
 def test_error_codes():
     w = configs.small(grid=(2, 3), cycles=4, mode="sparse", n_samples=8, n_slices=1, seed=5)
     ranks, labels, dims, data, opens = w.net.flat()

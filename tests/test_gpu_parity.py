@@ -174,6 +174,9 @@ ROUTES = {
                          "TN_REORDER": "1", "TN_REORDER_TOPK": "4"},
     "tc_reorder_none": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_SMALL": "2", "TN_TC_MIN_K": "2",
                         "TN_REORDER": "0"},
+    # big-output steps the general SIMT kernel would take, on the tensor cores with tiny K
+    "tc_small_k": {"TN_TC_MIN_BIG": "8", "TN_TC_MIN_K": "100000", "TN_TC_OUT_MIN": "1",
+                   "TN_TC_OUT_SIDE": "2", "TN_SKINNY_MIN_BIG": "100000"},
     "default": {},
 }
 
@@ -212,6 +215,10 @@ def test_contraction_vs_oracle(ctx, mode, route, monkeypatch):
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
         assert any(s["dense_merge"] for s in c.plan_json()["steps"])
+    if route == "tc_small_k":
+        c = Contraction(device=-1)
+        c.setup(w.net, w.samples, w.path, w.sliced)
+        assert any(s["route"] == "tcgen05" and s["k"] < 16 for s in c.plan_json()["steps"])
     if route == "tc_grouped" and mode == "sparse":
         c = Contraction(device=-1)
         c.setup(w.net, w.samples, w.path, w.sliced)
@@ -329,6 +336,32 @@ def test_c4_bench_workload_sampled_subslice(ctx):
           f"({sum(s['planes_out'] for s in steps)} plane producers, {sum(s['folded'] for s in steps)} folded gates)")
     assert err <= EXT_TOL
     assert err2 <= EXT_TOL
+
+
+@pytest.mark.timeout(900)
+def test_c5_m20_sampled_subslice(ctx):
+    """C5 (Sycamore-53 m=20, the paper's largest circuit, L549-559) at full width: one
+    sub-slice of slice 0 of the cached order (extra bonds fixed) vs the oracle."""
+    from tnworkloads.network import fix_bonds
+    w = configs.c5()
+    fine, pc = _refine(w, 3e11)
+    extra = fine[len(w.sliced):]
+    sub = fix_bonds(w.net, {x: 0 for x in extra})
+    c = Contraction(device=0, stream=torch.cuda.current_stream())
+    c.setup(sub, w.samples, w.path, w.sliced)
+    c.contract(0, 1)
+    got = c.sum_slices_host()
+    info = c.info()
+    c.reset_accumulator()
+    c.contract(0, 1)                       # fused planes + graph replay
+    got2 = c.sum_slices_host()
+    c.close()
+    ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
+    err, err2 = rel_l2(got, ref), rel_l2(got2, ref)
+    print(f"C5 sub-slice: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
+          f"tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}; fused pass {err2:.3e}")
+    assert info["n_tc_steps"] > 10
+    assert err <= EXT_TOL and err2 <= EXT_TOL
 
 
 @pytest.mark.timeout(900)

@@ -123,6 +123,24 @@ def c4(boundary: str = "single", peak: int = 32, tag: str = "a64") -> Workload:
     return w
 
 
+def c5(boundary: str = "single", peak: int = 32, tag: str = "a64") -> Workload:
+    """C5: Sycamore-53 m=20 (the paper's largest circuit, Table 5: per-slice
+    peak 2^32 elements = 32 GB complex64, L556) with a cached SA + dynamic-slicing order
+    file (tools/make_orders.py c5 --cycles 20 ...)."""
+    w = c4_base(boundary, cycles=20)
+    fn = _order_file(f"c5_{boundary}_p{peak}{tag}")
+    if not os.path.exists(fn):
+        raise FileNotFoundError(f"{fn} missing: run tools/make_orders.py c5 --cycles 20 --peak {peak} "
+                                f"--boundary {boundary} --alpha 64 --tag {tag}")
+    with open(fn) as f:
+        d = json.load(f)
+    w.path = [tuple(p) for p in d["path"]]
+    w.sliced = list(d["sliced"])
+    w.meta.update(d.get("meta", {}))
+    w.name = f"c5_sycamore53_m20_{boundary}_p{peak}{tag}"
+    return w
+
+
 def c3(samples_log2: int = 16, peak: int = 30, tag: str = "a64") -> Workload:
     """C3: Sycamore-53 m=14 with a sparse-state boundary of 2^samples_log2 uniform
     random bitstrings (stand-ins for experiment samples, L501) — the sparse einsum
