@@ -267,6 +267,14 @@ __device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, 
   }
 }
 
+// shared-memory load through an explicit ld.shared (the column table is reached through a
+// pointer the compiler cannot prove shared, which costs a generic LD per column)
+__device__ __forceinline__ int64_t lds64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
 // Tile index -> (j, mt, nt).  Tiles of one batch are visited in groups of
 // `group_m` tile rows, column-major inside a group, so the ~148 tiles resident
 // at once share few A and B panels in L2.
@@ -303,12 +311,18 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
                                      : Idesc<PAIR, FMT>::POS;
   const uint32_t IDESC_NEG = IDESC | (1u << 13);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1024-B aligned base by an offset into the shared array (not an integer round trip, which
+  // would hide the address space and turn every smem access through it into a generic one)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
+  // chunk accumulators in TMEM: 2 buffers of 256 columns (Cr | Ci, N = 128), or for narrow
+  // GEMMs (N <= 64) 4 buffers of 128 columns, two per epilogue half: the halves then
+  // drain alternate tiles (both busy, 4 chunks in flight) instead of half of the
+  // epilogue idling on the dead columns 64..127
   uint64_t* cfull = empty + STAGES;     // chunk accumulator ready (MMA -> epilogue)
-  uint64_t* cempty = cfull + 2;         // chunk accumulator drained (epilogue -> MMA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+  uint64_t* cempty = cfull + 4;         // chunk accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 4);
   // general output map: per-tile column offsets, double-buffered by tile parity
   int64_t* noff_tab = reinterpret_cast<int64_t*>(smem + STAGES * C::STAGE_BYTES + 256);
   float2* stage_buf = reinterpret_cast<float2*>(noff_tab + 2 * BN);   // [warp][32][9]
@@ -328,9 +342,11 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 4; ++s) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], PAIR ? 2 * EW : EW);   // pair: both CTAs' epilogue warps
+      // drained by every epilogue warp (narrow: by one half), of both CTAs for a pair
+      const int drainers = args.narrow ? EW / 2 : EW;
+      mbar_init(&cempty[s], PAIR ? 2 * drainers : drainers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&args.mapA)) : "memory");
@@ -425,18 +441,22 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       // (whole warp, converged; one elected lane issues each tcgen05 instruction)
       int stage = 0;
       uint32_t phase = 0;
-      int cb = 0;
-      uint32_t cphase = 0;
-      for (int64_t tile = unit; tile < args.n_tiles; tile += units) {
+      int cb = 0;                 // wide: next chunk buffer (0/1)
+      int hb = 0;                 // narrow: next buffer of each epilogue half's pair (bits 0, 1)
+      uint32_t bph = 0;           // phase bit of each chunk buffer
+      int b = 0;
+      int titer = 0;
+      for (int64_t tile = unit; tile < args.n_tiles; tile += units, ++titer) {
         for (int kb = 0; kb < kblocks; ++kb) {
           const int kin = kb % kchunk;
           if (kin == 0) {
+            b = args.narrow ? 2 * (titer & 1) + ((hb >> (titer & 1)) & 1) : cb;
             // chunk buffer drained by the epilogue (pair: by both CTAs')
-            mbar_wait(&cempty[cb], cphase ^ 1);   // pair: arrivals from both CTAs' epilogues
+            mbar_wait(&cempty[b], ((bph >> b) & 1u) ^ 1u);
             fence_after();
           }
-          const uint32_t d_re = tmem_base + cb * 256;
-          const uint32_t d_im = d_re + 128;
+          const uint32_t d_re = tmem_base + (args.narrow ? b * 128 : b * 256);
+          const uint32_t d_im = d_re + (args.narrow ? 64 : 128);
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint32_t st = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -501,11 +521,10 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
             phase ^= 1;
           }
           if (kin == kchunk - 1 || kb == kblocks - 1) {
-            mma_commit_t<PAIR>(&cfull[cb]);    // chunk accumulator ready for the epilogue(s)
-            if (++cb == 2) {
-              cb = 0;
-              cphase ^= 1;
-            }
+            mma_commit_t<PAIR>(&cfull[b]);     // chunk accumulator ready for the epilogue(s)
+            bph ^= 1u << b;
+            if (args.narrow) hb ^= 1 << (titer & 1);
+            else cb ^= 1;
           }
         }
       }
@@ -519,42 +538,69 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
     constexpr int WC = 512 / EW;
     const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
     const int half = (warp - EPI_WARP0) >> 2;
+    const int colh = args.narrow ? 0 : half;    // column half (narrow: the halves split tiles)
     const int row = quad * 32 + lane;
-    const float scale = ldexpf(1.0f, -(*args.scaleA + *args.scaleB));
+    // the operands carry 2^sA and 2^sB (|s| <= 120 each): 2^-(sA+sB) may leave the fp32
+    // range, so 2^-sA is folded into the chunk promotion and 2^-sB applied once per tile
+    const float scale = ldexpf(1.0f, -*args.scaleA);
+    const float scale_b = ldexpf(1.0f, -*args.scaleB);
     // fused plane output: consumer exponent sC = max(bound, delayed scaling); the planes
     // hold x * 2^sC = acc * 2^(sC - sA - sB)
     int plane_sc = 0;
     if (args.out_planes) {
       const int sab = *args.scaleA + *args.scaleB;
-      plane_sc = max(sab + args.plane_exp, *args.plane_pexp);
+      plane_sc = min(120, max(-120, max(sab + args.plane_exp, *args.plane_pexp)));
       if (blockIdx.x == 0 && threadIdx.x == 32 * EPI_WARP0) *args.plane_scale_out = plane_sc;
     }
     bool plane_ovf = false;
     float amax = 0.f;
-    int cb = 0;
-    uint32_t cphase = 0;
-    const uint32_t ce0 = PAIR ? map_rank(&cempty[0], 0) : 0;   // leader's drain barriers
-    const uint32_t ce1 = PAIR ? map_rank(&cempty[1], 0) : 0;
+    int cb = 0, eb = 0;
+    uint32_t bph = 0;                       // phase bit of each chunk buffer
     int titer = 0;
     int tab_nt = -1, tab_sel = 0;           // out_gen column table: tile column it holds
-    for (int64_t tile = unit; tile < args.n_tiles; tile += units, ++titer) {
+    // out_gen column offsets of tile column nt into the table buffer sel (all epilogue warps)
+    auto col_table = [&](int nt_, int sel) {
+      int64_t* tab = noff_tab + (sel & 1) * BN;
+      const int et = threadIdx.x - 32 * EPI_WARP0;
+      if (et < BN) {
+        int64_t t = (int64_t)nt_ * BN + et, off = 0;
+        for (int q = args.n_qo - 1; q >= 0; --q) {
+          const int sh = args.qo_sh[q];
+          off += (t & ((int64_t(1) << sh) - 1)) * args.qo_str[q];
+          t >>= sh;
+        }
+        tab[et] = off;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
+    };
+    if (args.narrow && args.out_gen) {      // one tile column: the table once, before the halves part
+      tab_nt = 0;
+      tab_sel = 1;
+      col_table(0, tab_sel);
+    }
+    const int64_t t_first = unit + (args.narrow ? half * units : 0);
+    const int64_t t_step = args.narrow ? 2 * units : units;
+    for (int64_t tile = t_first; tile < args.n_tiles; tile += t_step, ++titer) {
       int j, mt, nt;
       decode_tile(args, tile, j, mt, nt);
       float sr[WC], si[WC];
 #pragma unroll
       for (int i = 0; i < WC; ++i) { sr[i] = 0.f; si[i] = 0.f; }
       // column half entirely beyond N (narrow GEMMs): nothing to drain, only release
-      const bool cols_live = (int)(nt * BN + half * WC) < args.N;
+      const bool cols_live = (int)(nt * BN + colh * WC) < args.N;
       for (int ch = 0; ch < nchunks; ++ch) {
-        mbar_wait(&cfull[cb], cphase);
+        const int b = args.narrow ? 2 * half + eb : cb;
+        mbar_wait(&cfull[b], (bph >> b) & 1u);
         fence_after();
-        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + cb * 256 + half * WC;
+        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) +
+                            (args.narrow ? b * 128 : b * 256 + half * WC);
+        const uint32_t im_off = args.narrow ? 64 : 128;
         if (cols_live) {
 #pragma unroll
           for (int c = 0; c < WC / 32; ++c) {
             uint32_t vr[32], vi[32];
             TN_LD32(vr, tb + c * 32);
-            TN_LD32(vi, tb + 128 + c * 32);
+            TN_LD32(vi, tb + im_off + c * 32);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) {     // fp32 round-to-nearest promotion of the chunk,
@@ -567,33 +613,26 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
         fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (PAIR) mbar_arrive_remote(cb ? ce1 : ce0);
-          else mbar_arrive(&cempty[cb]);
+          if constexpr (PAIR) mbar_arrive_remote(map_rank(&cempty[b], 0));   // the leader's barrier
+          else mbar_arrive(&cempty[b]);
         }
-        if (++cb == 2) {
-          cb = 0;
-          cphase ^= 1;
-        }
+        bph ^= 1u << b;
+        if (args.narrow) eb ^= 1;
+        else cb ^= 1;
       }
+#pragma unroll
+      for (int i = 0; i < WC; ++i) { sr[i] *= scale_b; si[i] *= scale_b; }
       int m = mt * C::TILE_M + (int)rank * BM + row;
-      const int n0 = nt * BN + half * WC;
+      const int n0 = nt * BN + colh * WC;
       if (args.out_gen) {
         // ---- general output map: column offsets of this tile into smem (recomputed only
         // when the tile column changes; double-buffered), then stores
-        const bool new_nt = nt != tab_nt;
-        if (new_nt) { tab_nt = nt; ++tab_sel; }
-        int64_t* tab = noff_tab + (tab_sel & 1) * BN;
-        const int et = threadIdx.x - 32 * EPI_WARP0;     // epilogue thread 0 .. 32*EW-1
-        if (new_nt && et < BN) {
-          int64_t t = (int64_t)nt * BN + et, off = 0;
-          for (int q = args.n_qo - 1; q >= 0; --q) {
-            const int sh = args.qo_sh[q];
-            off += (t & ((int64_t(1) << sh) - 1)) * args.qo_str[q];
-            t >>= sh;
-          }
-          tab[et] = off;
+        if (nt != tab_nt) {
+          tab_nt = nt;
+          ++tab_sel;
+          col_table(nt, tab_sel);
         }
-        if (new_nt) asm volatile("bar.sync 1, %0;" ::"r"(32 * EW) : "memory");
+        int64_t* tab = noff_tab + (tab_sel & 1) * BN;
         if (args.out_planes) {
           // ---- fused consumer prep: 8 destination-contiguous columns -> one 16-B vector
           // per fp16 plane (RN hi, RN lo = rn(x - hi), Eq. 8), scaled by 2^plane_exp
@@ -606,7 +645,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
               t >>= sh;
             }
             const int64_t rb = m < args.M ? (int64_t)j * args.M * (int64_t)args.N + moff : -1;
-            const int64_t* tc = tab + half * WC;
+            const int64_t* tc = tab + colh * WC;
             __half* P = reinterpret_cast<__half*>(args.C);
             const int64_t pe = args.plane_elems;
             const float ps = ldexpf(1.0f, plane_sc);
@@ -638,7 +677,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
                 }
                 __syncwarp();
                 if (gb >= 0 && n0 + i + cc < args.N) {
-                  const int64_t a0 = gb + tc[i + cc];
+                  const int64_t a0 = gb + lds64(tc + i + cc);
                   *reinterpret_cast<uint4*>(P + a0) = *reinterpret_cast<const uint4*>(hr);
                   *reinterpret_cast<uint4*>(P + pe + a0) = *reinterpret_cast<const uint4*>(hi);
                   if (args.out_nplanes == 4) {
@@ -652,7 +691,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
 #pragma unroll
             for (int i = 0; i < WC; i += 8) {
               if (n0 + i >= args.N) continue;
-              const int64_t a0 = rb + tc[i];
+              const int64_t a0 = rb + lds64(tc + i);
               __align__(16) __half hr[8], hi[8], lr[8], li[8];
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {
@@ -682,7 +721,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
             moff += (t & ((int64_t(1) << sh) - 1)) * args.po_str[q];
             t >>= sh;
           }
-          const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff + tab[half * WC];
+          const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff + lds64(tab + colh * WC);
           store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C, rb, m < args.M,
                                 lane, amax);
           continue;
@@ -695,7 +734,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
             t >>= sh;
           }
           const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff;
-          const int64_t* tc = tab + half * WC;
+          const int64_t* tc = tab + colh * WC;
           if (args.cols_stride > 1) {
             // one strided column dim (the consumer's unit-stride dim is a row dim): a
             // column's offset is n * stride, no table reads or contiguity tests
@@ -713,11 +752,11 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
           for (int i = 0; i < WC; i += 2) {      // full unroll: sr/si stay in registers
             if (n0 + i >= args.N) continue;
             const float r0 = sr[i], i0 = si[i];
-            const int64_t a0 = rb + tc[i];
+            const int64_t a0 = rb + lds64(tc + i);
             amax = fmaxf(amax, fmaxf(fabsf(r0), fabsf(i0)));
             if (n0 + i + 1 < args.N) {
               const float r1 = sr[i + 1], i1 = si[i + 1];
-              const int64_t a1 = rb + tc[i + 1];
+              const int64_t a1 = rb + lds64(tc + i + 1);
               amax = fmaxf(amax, fmaxf(fabsf(r1), fabsf(i1)));
               if (a1 == a0 + 1 && (a0 & 1) == 0) {
                 *reinterpret_cast<float4*>(args.C + a0) = make_float4(r0, i0, r1, i1);

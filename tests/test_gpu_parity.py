@@ -341,25 +341,42 @@ def test_c4_bench_workload_sampled_subslice(ctx):
 @pytest.mark.timeout(900)
 def test_c5_m20_sampled_subslice(ctx):
     """C5 (Sycamore-53 m=20, the paper's largest circuit, L549-559) at full width: one
-    sub-slice of slice 0 of the cached order (extra bonds fixed) vs the oracle."""
-    from tnworkloads.network import fix_bonds
+    sub-slice of the cached order (45 extra bonds fixed) vs the oracle.
+
+    The digits of the 43 sliced and 45 extra bonds are seeded-random, not all 0: with
+    every digit 0 this order's sub-slices are structurally zero (two fp64 paths of the
+    oracle disagree at the 1e-54 level and a complex64 evaluation returns noise), which
+    no relative bound can test.  Seed 102 gives |amp| ~ 2e-21, for which a complex64
+    evaluation of the same path agrees with fp64 to 9e-7."""
+    from tnworkloads.network import Network, fix_bonds
     w = configs.c5()
     fine, pc = _refine(w, 3e11)
     extra = fine[len(w.sliced):]
-    sub = fix_bonds(w.net, {x: 0 for x in extra})
+    rng = np.random.default_rng(102)
+    digit = {x: int(rng.integers(w.net.dims[x])) for x in fine}
+    sub = fix_bonds(w.net, {x: digit[x] for x in extra})
+    t = 0
+    for x in w.sliced:                     # mixed radix, last sliced bond fastest
+        t = t * w.net.dims[x] + digit[x]
+    ref0 = oracle.contract_slice(sub, w.path, w.sliced, t, w.samples)
+    # the contraction is multilinear: scale every tensor by c = |ref|^(-1/N) so the
+    # result is O(1) and no complex64 intermediate nears the subnormal range
+    c_ = float(np.abs(ref0).max()) ** (-1.0 / sub.n_tensors)
+    sub = Network([tt * c_ for tt in sub.tensors], sub.labels, sub.dims, sub.open_labels, sub.n_qubits,
+                  sub.coords)
+    ref = ref0 * c_ ** sub.n_tensors
     c = Contraction(device=0, stream=torch.cuda.current_stream())
     c.setup(sub, w.samples, w.path, w.sliced)
-    c.contract(0, 1)
+    c.contract(t, t + 1)
     got = c.sum_slices_host()
     info = c.info()
     c.reset_accumulator()
-    c.contract(0, 1)                       # fused planes + graph replay
+    c.contract(t, t + 1)                   # fused planes + graph replay
     got2 = c.sum_slices_host()
     c.close()
-    ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
     err, err2 = rel_l2(got, ref), rel_l2(got2, ref)
-    print(f"C5 sub-slice: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
-          f"tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}; fused pass {err2:.3e}")
+    print(f"C5 sub-slice: slice {t}, extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
+          f"|ref0| {abs(ref0[0]):.3g}, tc steps {info['n_tc_steps']}, rel_l2 {err:.3e}; fused pass {err2:.3e}")
     assert info["n_tc_steps"] > 10
     assert err <= EXT_TOL and err2 <= EXT_TOL
 
