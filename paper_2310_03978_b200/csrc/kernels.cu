@@ -625,6 +625,186 @@ __global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __res
   }
 }
 
+// Tensor-core variant of the gate-folded prep (K = 4, 8, 16 and N <= 8 * NB): the small
+// contraction out[carry][n] = Σ_k X[carry][k] Y[n][k] of a tile runs as warp-level
+// m16n8k16 fp16 MMAs with fp32 accumulation in the 3-pass hi/lo split of Eq. 8
+// (X and Y each carry their own power-of-two scale) and the complex
+// product as four real ones (Cr = Xr Yr - Xi Yi, Ci = Xr Yi + Xi Yr).  The FFMA kernel
+// above spends 4 K FFMA per output element (32 for K = 8): it is issue-bound on the
+// 2^32-element stem operands; here a warp issues 12 MMAs per 16 x 8 outputs.  Y's
+// fragments stay in registers for the whole kernel.
+__device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
+  return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+}
+__device__ __forceinline__ void split_h(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <int PLANES, int KT, int NB>
+__global__ void __launch_bounds__(256, 2) prep_gate_mma_kernel(const PrepDesc* __restrict__ gd,
+                                                               const int64_t* __restrict__ leaf_off) {
+  static_assert(KT == 4 || KT == 8 || KT == 16, "K padded to one m16n8k16 step");
+  __shared__ __align__(16) PrepDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  float2* buf = reinterpret_cast<float2*>(dyn);                      // [GP_BUF] X tile
+  float2* obuf = buf + GP_BUF;                                        // [GP_BUF] padded outputs
+  float2* Ys = obuf + GP_BUF;                                         // [N][KT]
+  int64_t* s_src = reinterpret_cast<int64_t*>(Ys + GP_YMAX);          // [128]
+  int64_t* s_dst = s_src + 128;                                       // [TD/8]
+  uint16_t* s_fc = reinterpret_cast<uint16_t*>(s_dst + GP_TMAX / 8);  // [2^cb]
+  uint16_t* s_fn = s_fc + GP_TMAX;                                    // [N]
+  const int TD = 1 << d.bp_t, TS = 1 << d.g_ts, N = d.g_N, CB = 1 << d.g_cbits;
+  {
+    const int64_t* tab = d.bp_tab;
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) s_src[i] = tab[i];
+    for (int i = threadIdx.x; i < TD / 8; i += blockDim.x) s_dst[i] = tab[128 + i];
+    const uint16_t* fc = reinterpret_cast<const uint16_t*>(tab + 128 + TD / 8);
+    for (int i = threadIdx.x; i < CB; i += blockDim.x) s_fc[i] = fc[i];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_fn[i] = fc[GP_TMAX + i];
+    const float2* Y = d.gy + d.gy_off + (d.gy_leaf >= 0 ? leaf_off[d.gy_leaf] : 0);
+    for (int e = threadIdx.x; e < N * KT; e += blockDim.x) {
+      const int n = e / KT, k = e % KT;
+      Ys[e] = Y[decompose(n, d.g_nn, d.gy_n_ext, d.gy_n_s) + decompose(k, d.g_nk, d.gy_k_ext, d.gy_k_s)];
+    }
+  }
+  const float2* src = d.src + d.off + (d.leaf >= 0 ? leaf_off[d.leaf] : 0);
+  // scales: X and Y to the fp16 range (each |.| * 2^s < 2^15), the planes as the FFMA kernel
+  const float ax = __uint_as_float(*d.absmax_in), ay = __uint_as_float(*d.absmax_y);
+  auto exp15 = [](float a) {
+    int e = 0;
+    if (a > 0.f) frexpf(a, &e);
+    return a > 0.f ? max(-120, min(120, 15 - e)) : 0;
+  };
+  const int sx = exp15(ax), sy = exp15(ay);
+  float scale;
+  {
+    const float bound = 2.f * (float)KT * ax * ay;
+    const int s = exp15(bound);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *d.scale_out = s;
+    scale = ldexpf(1.0f, s);
+  }
+  const float fx = ldexpf(1.0f, sx), fy = ldexpf(1.0f, sy);
+  const float ux = ldexpf(1.0f, -sx), uy = ldexpf(1.0f, -sy);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  // B fragments (k x n, col): b0 = k {2t, 2t+1}, b1 = k {2t+8, 2t+9}, column n = 8 nb + g
+  // of Yr, Yi and -Yi, each split hi / lo
+  uint32_t bf[NB][6][2];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    const int n = nb * 8 + g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      __half rh[2], rl[2], ih[2], il[2], nh[2], nl[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = 2 * t + 8 * h + u;
+        const float2 y = (n < N && k < KT) ? Ys[n * KT + k] : make_float2(0.f, 0.f);
+        split_h(y.x * fy, rh[u], rl[u]);
+        split_h(y.y * fy, ih[u], il[u]);
+        split_h(-y.y * fy, nh[u], nl[u]);
+      }
+      bf[nb][0][h] = pack_h2(rh[0], rh[1]);
+      bf[nb][1][h] = pack_h2(rl[0], rl[1]);
+      bf[nb][2][h] = pack_h2(ih[0], ih[1]);
+      bf[nb][3][h] = pack_h2(il[0], il[1]);
+      bf[nb][4][h] = pack_h2(nh[0], nh[1]);
+      bf[nb][5][h] = pack_h2(nl[0], nl[1]);
+    }
+  }
+  const bool vec = d.bp_vec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  const int nrb = CB / 16;
+  for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
+    int64_t sc = 0, dc = 0;
+    for (int i = 0; i < d.nc; ++i)
+      if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
+    __syncthreads();   // previous tile's outputs consumed
+    const float2* sp = src + sc;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 512; ++i) {
+        const int e = 2 * (threadIdx.x + i * 256);
+        if (e < TS) cp_async16(buf + e, sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < GP_TMAX / 256; ++i) {
+        const int e = threadIdx.x + i * 256;
+        if (e < TS) cp_async8(buf + e, sp + s_src[e & 63] + s_src[64 + (e >> 6)]);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // per 16-carry row block of this warp: A fragments from the X tile (element (carry, k)
+    // at buf[carry + k*CB]; a0 = (g, k 2t..2t+1), a1 = (g+8, ..), a2 = (g, k+8), a3 = (g+8,
+    // k+8)), 12 MMAs per 8 output columns, outputs into the padded output tile
+    for (int rb = warp; rb < nrb; rb += 8) {
+      uint32_t af[4][4];                        // [Xr_h, Xr_l, Xi_h, Xi_l][reg]
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = rb * 16 + g + ((r & 1) ? 8 : 0);
+        const int k0 = 2 * t + ((r & 2) ? 8 : 0);
+        __half xrh[2], xrl[2], xih[2], xil[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = k0 + u;
+          const float2 x = k < KT ? buf[row + k * CB] : make_float2(0.f, 0.f);
+          split_h(x.x * fx, xrh[u], xrl[u]);
+          split_h(x.y * fx, xih[u], xil[u]);
+        }
+        af[0][r] = pack_h2(xrh[0], xrh[1]);
+        af[1][r] = pack_h2(xrl[0], xrl[1]);
+        af[2][r] = pack_h2(xih[0], xih[1]);
+        af[3][r] = pack_h2(xil[0], xil[1]);
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        float cr[4] = {0.f, 0.f, 0.f, 0.f}, ci[4] = {0.f, 0.f, 0.f, 0.f};
+        // small terms first, big x big last (Eq. 8)
+        mma16816(cr, af[0], bf[nb][1]);   // Xr_h Yr_l
+        mma16816(cr, af[1], bf[nb][0]);   // Xr_l Yr_h
+        mma16816(cr, af[2], bf[nb][5]);   // Xi_h (-Yi)_l
+        mma16816(cr, af[3], bf[nb][4]);   // Xi_l (-Yi)_h
+        mma16816(ci, af[0], bf[nb][3]);   // Xr_h Yi_l
+        mma16816(ci, af[1], bf[nb][2]);   // Xr_l Yi_h
+        mma16816(ci, af[2], bf[nb][1]);   // Xi_h Yr_l
+        mma16816(ci, af[3], bf[nb][0]);   // Xi_l Yr_h
+        mma16816(cr, af[0], bf[nb][0]);   // Xr_h Yr_h
+        mma16816(cr, af[2], bf[nb][4]);   // Xi_h (-Yi)_h
+        mma16816(ci, af[0], bf[nb][2]);   // Xr_h Yi_h
+        mma16816(ci, af[2], bf[nb][0]);   // Xi_h Yr_h
+        // c0, c1: (row g, n 2t, 2t+1); c2, c3: (row g+8, ...)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = rb * 16 + g + ((r & 2) ? 8 : 0);
+          const int n = nb * 8 + 2 * t + (r & 1);
+          if (n < N) {
+            const int f = s_fc[row] + s_fn[n];
+            obuf[f + (f >> 5)] = make_float2(cr[r] * ux * uy, ci[r] * ux * uy);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
+      float2 o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = obuf[8 * q + j + ((8 * q) >> 5)];
+      split_store8<PLANES>(d, dc + s_dst[q], o, scale);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- SIMT einsum, general
 // One thread per output C[j][m][n]; fp64 accumulation (a long fp32 RN chain would
 // cost ~2^-24·sqrt(K/2) relative).
@@ -1398,6 +1578,15 @@ cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int PLANES, int KT, int NB>
+cudaError_t launch_gate_mma_t(const PrepDesc* d_desc, int g, const int64_t* leaf_off, cudaStream_t s) {
+  const void* k = reinterpret_cast<const void*>(prep_gate_mma_kernel<PLANES, KT, NB>);
+  constexpr size_t smem = GP_SMEM + GP_BUF * 8;     // + the separate output tile
+  if (cudaError_t e = set_smem_attr(k, (int)smem)) return e;
+  prep_gate_mma_kernel<PLANES, KT, NB><<<g, 256, smem, s>>>(d_desc, leaf_off);
+  return cudaGetLastError();
+}
+
 template <int PLANES, int KT>
 cudaError_t launch_gate_t(const PrepDesc* d_desc, int g, const int64_t* leaf_off, cudaStream_t s) {
   if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(prep_gate_kernel<PLANES, KT>), (int)GP_SMEM))
@@ -1422,12 +1611,31 @@ cudaError_t launch_gate(const PrepDesc* d_desc, int planes, int k, int g, const 
 }
 
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
-                        const int64_t* leaf_off, cudaStream_t s, int gate_k) {
+                        const int64_t* leaf_off, cudaStream_t s, int gate_k, int gate_n) {
   const int th = 256;
   if (kind == 5) {   // gate-folded prep (K = 1, 2, 4, 8 or 16, carried in the descriptor)
     const int64_t tiles = total / std::max(tile_T, 1);
     const int bps = g_knobs.gate_bps;
     const int g = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * bps);
+    // TN_GATE_MMA=1, K >= 4 and N <= 32: warp-level tensor-core MMAs (off by default: on
+    // C4 it ran 33 ms where the FFMA kernel runs 24 ms)
+    if (g_knobs.gate_mma && gate_k >= 4 && gate_n >= 1 && gate_n <= 32) {
+      const int gm = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 2);
+#define TN_GMMA(P, KT)                                                                       \
+  (gate_n <= 8 ? launch_gate_mma_t<P, KT, 1>(d_desc, gm, leaf_off, s)                        \
+               : gate_n <= 16 ? launch_gate_mma_t<P, KT, 2>(d_desc, gm, leaf_off, s)         \
+                              : launch_gate_mma_t<P, KT, 4>(d_desc, gm, leaf_off, s))
+      if (planes == 4) {
+        if (gate_k == 4) return TN_GMMA(4, 4);
+        if (gate_k == 8) return TN_GMMA(4, 8);
+        if (gate_k == 16) return TN_GMMA(4, 16);
+      } else {
+        if (gate_k == 4) return TN_GMMA(2, 4);
+        if (gate_k == 8) return TN_GMMA(2, 8);
+        if (gate_k == 16) return TN_GMMA(2, 16);
+      }
+#undef TN_GMMA
+    }
     return launch_gate(d_desc, planes, gate_k, g, leaf_off, s);
   }
   if (kind == 4) {   // bit-permutation transposer, tiles of tile_T <= 4096 elements
@@ -1725,6 +1933,7 @@ void refresh_knobs() {
   k.simt_old = env_or("TN_SIMT_OLD", 0);
   k.skinny_vec2 = env_or("TN_SKINNY_VEC2", 1);
   k.narrow_mma = env_or("TN_NARROW_MMA", 1);
+  k.gate_mma = env_or("TN_GATE_MMA", 0);   // measured slower than the FFMA kernel
   k.prep_bp = env_or("TN_PREP_BP", 1);
   k.pair_min_m = env_or("TN_GEMM_PAIR_MIN_M", 512);
   g_knobs = k;

@@ -110,6 +110,7 @@ struct StepPlan {
   // the step whose planes this step's epilogue writes (-1: writes complex64)
   bool skip_prep[2] = {false, false};
   int gate_k[2] = {0, 0};       // gate-folded prep: K of the folded gate per side
+  int gate_n[2] = {0, 0};       // ... and its N (outputs per carry position)
   int planes_consumer = -1;
   tn::GemmArgs gemm_plain;      // the step's GEMM without fusion (first, absmax-seeding slice)
 };
@@ -1936,6 +1937,7 @@ tn_status build_plan(tn_ctx* c) {
         cs.r_fast[side] = 5;
         cs.gtT[side] = trial.T;
         cs.gate_k[side] = (int)pp.hdesc.K;
+        cs.gate_n[side] = (int)pp.hdesc.N;
         gate_ref.push_back({cs.prep_idx + side, (int64_t)gt_all.size()});
         gt_all.insert(gt_all.end(), tab.begin(), tab.end());
         pp.folded = true;
@@ -2048,7 +2050,8 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
         if (fused && sp.skip_prep[side]) continue;   // planes written by the producer's epilogue
         Timer tm(c, 1, 0, (double)sp.prep_total[side] * (8.0 + 2.0 * planes), (int)s, sm);
         TN_CUDA(tn::launch_prep(c->d_prep + sp.prep_idx + side, sp.prep_total[side], planes,
-                                sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm, sp.gate_k[side]));
+                                sp.r_fast[side], sp.gtT[side], c->d_leaf_off, sm, sp.gate_k[side],
+                                sp.gate_n[side]));
       }
       tn::GemmArgs ga = fused ? sp.gemm : sp.gemm_plain;
       ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;

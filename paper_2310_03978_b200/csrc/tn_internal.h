@@ -164,6 +164,7 @@ struct Knobs {
   int skinny_rows = 0;    // TN_SKINNY_ROWS: force the skinny kernel's rows per thread (tests)
   int simt_old = 0;       // TN_SIMT_OLD: force the previous skinny design (A/B tests)
   int skinny_vec2 = 1;    // TN_SKINNY_VEC2=0: no paired-lane / k-pair 16-B accesses (tests)
+  int gate_mma = 0;       // TN_GATE_MMA=1: gate-folded preps with K >= 4 on mma.sync (measured slower)
   int narrow_mma = 1;     // TN_NARROW_MMA=0: N <= 64 GEMMs issue N = 128 MMAs (A/B tests)
   int prep_bp = 1;        // TN_PREP_BP=0: no bit-permutation transposer (A/B tests)
   int pair_min_m = 512;   // TN_GEMM_PAIR_MIN_M: CTA-pair GEMM from this M (0 = never)
@@ -181,7 +182,7 @@ int max_active_clusters(const void* kernel, const cudaLaunchConfig_t& cfg, int f
 cudaError_t launch_slice_select(const SliceDesc* d_desc, cudaStream_t s);
 cudaError_t launch_set_counter(int64_t* counter, int64_t value, cudaStream_t s);
 cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int kind, int tile_T,
-                        const int64_t* leaf_off, cudaStream_t s, int gate_k = 0);
+                        const int64_t* leaf_off, cudaStream_t s, int gate_k = 0, int gate_n = 0);
 // variant: kernel variant of the SIMT mode (0 = heuristic); einsum_variants() = how many
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
                           const int64_t* leaf_off, cudaStream_t s, int variant = 0);

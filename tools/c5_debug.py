@@ -1,5 +1,5 @@
-"""C5 sub-slice diagnosis: the scaled sub-network of test_c5_m20_sampled_subslice under
-several routing settings (one process per setting, env given on the command line)."""
+"""C5 sub-slice precision diagnosis: the seeded-digit sub-slice of
+test_c5_m20_sampled_subslice under the routing given in the environment."""
 import os
 import sys
 
@@ -15,13 +15,21 @@ from paper_2310_03978_b200 import Contraction  # noqa: E402
 
 w = configs.c5()
 fine, _ = refine_slices(w.net, w.samples, w.path, w.sliced, 3e11, max_extra=48)
-sub = fix_bonds(w.net, {x: 0 for x in fine[len(w.sliced):]})
-ref0 = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
+extra = fine[len(w.sliced):]
+rng = np.random.default_rng(102)
+digit = {x: int(rng.integers(w.net.dims[x])) for x in fine}
+sub = fix_bonds(w.net, {x: digit[x] for x in extra})
+t = 0
+for x in w.sliced:
+    t = t * w.net.dims[x] + digit[x]
+ref0 = oracle.contract_slice(sub, w.path, w.sliced, t, w.samples)
 c_ = float(np.abs(ref0).max()) ** (-1.0 / sub.n_tensors)
-sub = Network([t * c_ for t in sub.tensors], sub.labels, sub.dims, sub.open_labels, sub.n_qubits, sub.coords)
+sub = Network([tt * c_ for tt in sub.tensors], sub.labels, sub.dims, sub.open_labels, sub.n_qubits, sub.coords)
 ref = ref0 * c_ ** sub.n_tensors
 c = Contraction(device=0, stream=torch.cuda.current_stream())
 c.setup(sub, w.samples, w.path, w.sliced)
-c.contract(0, 1)
-got = c.sum_slices_host()
-print(os.environ.get("TAG", ""), "got", got, "ref", ref, "rel", float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
+for rep in range(2):
+    c.reset_accumulator()
+    c.contract(t, t + 1, os.environ.get("PREC", "extended"))
+    got = c.sum_slices_host()
+    print(os.environ.get("TAG", ""), rep, "rel", float(np.linalg.norm(got - ref) / np.linalg.norm(ref)), flush=True)
