@@ -636,66 +636,6 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
         if (args.out_planes) {
           // ---- fused consumer prep: 8 destination-contiguous columns -> one 16-B vector
           // per fp16 plane (RN hi, RN lo = rn(x - hi), Eq. 8), scaled by 2^plane_exp
-          if (EW == 8 && !args.planes_rows && n0 < args.N) {
-            // unit-stride plane dim = the 8 lowest column bits: per 32 columns and plane, the
-            // warp stages its 32 rows x 64 B in smem, then each store instruction writes 32
-            // consecutive 16-B chunks (4 chunks per row, 8 rows): when the block of 32 rows x
-            // 32 columns is contiguous in the consumer's planes (the usual case) that is
-            // 512 contiguous bytes instead of 32 scattered 16-B halves of sectors
-            int64_t t = m < args.M ? m : 0, moff = 0;
-            for (int q = args.n_po - 1; q >= 0; --q) {
-              const int sh = args.po_sh[q];
-              moff += (t & ((int64_t(1) << sh) - 1)) * args.po_str[q];
-              t >>= sh;
-            }
-            const int64_t rb = m < args.M ? (int64_t)j * args.M * (int64_t)args.N + moff : -1;
-            const int64_t* tc = tab + colh * WC;
-            __half* P = reinterpret_cast<__half*>(args.C);
-            const int64_t pe = args.plane_elems;
-            const float ps = ldexpf(1.0f, plane_sc);
-            uint16_t* sb = reinterpret_cast<uint16_t*>(stage_buf + (warp - EPI_WARP0) * 32 * 10);
-            const int nplanes = args.out_nplanes;
-#pragma unroll
-            for (int c0 = 0; c0 < WC; c0 += 32) {
-              if (n0 + c0 >= args.N) break;
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj) {
-                if (rb >= 0 && n0 + c0 + jj < args.N) {
-                  amax = fmaxf(amax, fmaxf(fabsf(sr[c0 + jj]), fabsf(si[c0 + jj])));
-                  plane_ovf |= fmaxf(fabsf(sr[c0 + jj] * ps), fabsf(si[c0 + jj] * ps)) >= 65504.f;
-                }
-              }
-              for (int pl = 0; pl < nplanes; ++pl) {
-                // plane pl of this lane's 32 columns: 0 re_hi, 1 im_hi, 2 re_lo, 3 im_lo (Eq. 8 RN)
-                uint32_t v[16];
-#pragma unroll
-                for (int jj = 0; jj < 16; ++jj) {
-                  __half h2[2];
-#pragma unroll
-                  for (int u = 0; u < 2; ++u) {
-                    const float x = ((pl & 1) ? si[c0 + 2 * jj + u] : sr[c0 + 2 * jj + u]) * ps;
-                    const __half hh = __float2half_rn(x);
-                    h2[u] = pl < 2 ? hh : __float2half_rn(x - __half2float(hh));
-                  }
-                  v[jj] = (uint32_t)__half_as_ushort(h2[0]) | ((uint32_t)__half_as_ushort(h2[1]) << 16);
-                }
-                uint4* w = reinterpret_cast<uint4*>(sb + lane * 40);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) w[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const int r = 8 * i + (lane >> 2), cg = lane & 3;
-                  const int64_t rbr = __shfl_sync(0xffffffffu, rb, r);
-                  const uint4 val = reinterpret_cast<const uint4*>(sb + r * 40)[cg];
-                  if (rbr >= 0 && n0 + c0 + 8 * cg < args.N)
-                    *reinterpret_cast<uint4*>(P + pl * pe + rbr + lds64(tc + c0 + 8 * cg)) = val;
-                }
-                __syncwarp();
-              }
-            }
-            continue;
-          }
           if (n0 < args.N && (m < args.M || (EW == 8 && args.planes_rows))) {
             // rows mode: M is a multiple of 8 row groups, so a group is all-valid or all-padding
             int64_t t = m < args.M ? m : 0, moff = 0;
