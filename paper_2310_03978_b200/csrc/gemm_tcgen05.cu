@@ -147,6 +147,26 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* dst, u
       : "memory");
 }
 
+// operand loads with an L2 eviction-priority hint (evict_last: the A / B panels are
+// re-read by the other column / row tiles of their wave, while the output streams
+// past them through L2)
+__device__ __forceinline__ void tma_load_4d_hint(const CUtensorMap* map, void* dst, uint64_t* bar, int c0,
+                                                 int c1, int c2, int c3, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair_hint(const CUtensorMap* map, void* dst, uint32_t bar_cluster,
+                                                      int c0, int c1, int c2, int c3, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+      : "memory");
+}
+
 // CTA-pair TMA: the destination is this CTA's smem, the completion goes to the
 // leader CTA's barrier (bar_cluster = its shared::cluster address)
 __device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, void* dst, uint32_t bar_cluster,
@@ -244,7 +264,7 @@ __device__ __forceinline__ void tmem_wait_ld() {
 template <int WC>
 __device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, const float* si,
                                                   float2* C, int64_t base, bool valid, int lane,
-                                                  float& amax) {
+                                                  float& amax, bool stream) {
   const unsigned vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
   for (int i = 0; i < WC; i += 8) {
@@ -261,7 +281,10 @@ __device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, 
       const int r = (lane >> 2) + 8 * q, c = lane & 3;
       const int64_t rb = __shfl_sync(0xffffffffu, base, r);
       const float4 v = reinterpret_cast<const float4*>(buf + r * 10)[c];
-      if ((vmask >> r) & 1u) *reinterpret_cast<float4*>(C + rb + i + 2 * c) = v;
+      if ((vmask >> r) & 1u) {
+        if (stream) __stcs(reinterpret_cast<float4*>(C + rb + i + 2 * c), v);   // evict-first
+        else *reinterpret_cast<float4*>(C + rb + i + 2 * c) = v;
+      }
     }
     __syncwarp();
   }
@@ -384,6 +407,8 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long target = 0;
+      uint64_t pol = 0;
+      if (args.l2hint) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
       const int per_unit = PAIR ? 2 : 1;
       for (int64_t tile = unit; tile < args.n_tiles; tile += units) {
         if (args.wave_sync) {
@@ -411,22 +436,42 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
           if constexpr (PAIR) {
             const uint32_t fb = map_rank(&full[stage], 0);
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if (args.l2hint) {
 #pragma unroll
-            for (int p = 0; p < PLANES; ++p)
-              tma_load_4d_pair(&args.mapA, st + p * PLANE_TILE, fb, kb * BKE, arow, sa, p);
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d_pair_hint(&args.mapA, st + p * PLANE_TILE, fb, kb * BKE, arow, sa, p, pol);
 #pragma unroll
-            for (int p = 0; p < PLANES; ++p)
-              tma_load_4d_pair(&args.mapB2, st + PLANES * PLANE_TILE + p * C::B_TILE, fb, kb * BKE,
-                               brow, sb, p);
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d_pair_hint(&args.mapB2, st + PLANES * PLANE_TILE + p * C::B_TILE, fb, kb * BKE,
+                                      brow, sb, p, pol);
+            } else {
+#pragma unroll
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d_pair(&args.mapA, st + p * PLANE_TILE, fb, kb * BKE, arow, sa, p);
+#pragma unroll
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d_pair(&args.mapB2, st + PLANES * PLANE_TILE + p * C::B_TILE, fb, kb * BKE,
+                                 brow, sb, p);
+            }
           } else {
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            if (args.l2hint) {
 #pragma unroll
-            for (int p = 0; p < PLANES; ++p)
-              tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BKE, arow, sa, p);
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d_hint(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BKE, arow, sa, p, pol);
 #pragma unroll
-            for (int p = 0; p < PLANES; ++p)
-              tma_load_4d(&args.mapB, st + PLANES * PLANE_TILE + p * C::B_TILE, &full[stage],
-                          kb * BKE, brow, sb, p);
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d_hint(&args.mapB, st + PLANES * PLANE_TILE + p * C::B_TILE, &full[stage],
+                                 kb * BKE, brow, sb, p, pol);
+            } else {
+#pragma unroll
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d(&args.mapA, st + p * PLANE_TILE, &full[stage], kb * BKE, arow, sa, p);
+#pragma unroll
+              for (int p = 0; p < PLANES; ++p)
+                tma_load_4d(&args.mapB, st + PLANES * PLANE_TILE + p * C::B_TILE, &full[stage],
+                            kb * BKE, brow, sb, p);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -723,7 +768,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
           }
           const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff + lds64(tab + colh * WC);
           store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C, rb, m < args.M,
-                                lane, amax);
+                                lane, amax, args.l2hint != 0);
           continue;
         }
         if (m < args.M && n0 < args.N) {
@@ -810,7 +855,8 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
       if (EW == 8 && !args.acc && (args.N % 2) == 0 && n0 + WC <= args.N) {
         store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C,
-                              orow * (int64_t)args.N + n0, m < args.M && orow >= 0, lane, amax);
+                              orow * (int64_t)args.N + n0, m < args.M && orow >= 0, lane, amax,
+                              args.l2hint != 0);
         continue;
       }
       if (m < args.M && n0 < args.N && orow >= 0) {
@@ -952,6 +998,7 @@ bool gemm_pair_ok(const GemmArgs& a, int min_m) {
 cudaError_t launch_gemm(const GemmArgs& a_in, int passes, int num_sms, cudaStream_t s, int format) {
   GemmArgs a = a_in;
   a.narrow = (g_knobs.narrow_mma && a.N <= 64) ? 1 : 0;
+  a.l2hint = g_knobs.l2hint;
   if (a.wave_sync) {
     cudaError_t e = cudaMemsetAsync(a.wave_ctr, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;

@@ -120,6 +120,7 @@ struct GemmArgs {
   // with plane_exp = -16 - ceil(log2 K): |acc| <= K 2^31 for operands scaled below 2^15,
   // so the planes stay below 2^15 without waiting for the output's absmax; the consumer's
   // exponent sA + sB + plane_exp goes to *plane_scale_out.
+  int32_t l2hint;                 // 1: operand TMA loads carry an L2 evict_last policy
   int32_t out_planes, out_nplanes, plane_exp;
   int32_t planes_rows;            // 1: the unit-stride plane dim is the 8 lowest row bits
                                   // (staged through smem); 0: the 8 lowest column bits
@@ -165,6 +166,7 @@ struct Knobs {
   int simt_old = 0;       // TN_SIMT_OLD: force the previous skinny design (A/B tests)
   int skinny_vec2 = 1;    // TN_SKINNY_VEC2=0: no paired-lane / k-pair 16-B accesses (tests)
   int gate_mma = 0;       // TN_GATE_MMA=1: gate-folded preps with K >= 4 on mma.sync (measured slower)
+  int l2hint = 1;         // TN_GEMM_L2HINT=0: operand TMA loads without the evict_last policy
   int narrow_mma = 1;     // TN_NARROW_MMA=0: N <= 64 GEMMs issue N = 128 MMAs (A/B tests)
   int prep_bp = 1;        // TN_PREP_BP=0: no bit-permutation transposer (A/B tests)
   int pair_min_m = 512;   // TN_GEMM_PAIR_MIN_M: CTA-pair GEMM from this M (0 = never)
