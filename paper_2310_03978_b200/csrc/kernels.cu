@@ -1933,7 +1933,7 @@ void refresh_knobs() {
   k.simt_old = env_or("TN_SIMT_OLD", 0);
   k.skinny_vec2 = env_or("TN_SKINNY_VEC2", 1);
   k.narrow_mma = env_or("TN_NARROW_MMA", 1);
-  k.l2hint = env_or("TN_GEMM_L2HINT", 1);
+  k.l2hint = env_or("TN_GEMM_L2HINT", 0);   // measured neutral
   k.gate_mma = env_or("TN_GATE_MMA", 0);   // measured slower than the FFMA kernel
   k.prep_bp = env_or("TN_PREP_BP", 1);
   k.pair_min_m = env_or("TN_GEMM_PAIR_MIN_M", 512);

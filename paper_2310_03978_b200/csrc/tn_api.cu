@@ -141,6 +141,7 @@ struct tn_ctx {
   int num_sms = 148;
   // k-blocks per promoted TMEM chunk: 3-pass / 1-pass
   int kchunk3 = 1, kchunk1 = 0;
+  int kchunk3_short = 1, shortk_max = 16;
   int group_m = 16;             // GEMM tile rasterization group (tile rows)
   bool autotune = true;         // TN_AUTOTUNE=0: SIMT steps use the heuristic kernel variant
   // CUDA graph of one slice's launch sequence (TN_GRAPHS=0 disables)
@@ -2055,6 +2056,9 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
       }
       tn::GemmArgs ga = fused ? sp.gemm : sp.gemm_plain;
       ga.kchunk = ps == 3 ? c->kchunk3 : c->kchunk1;
+      // short-K 3-pass GEMMs (K <= 32 * shortk_max): promote every kchunk3_short k-blocks
+      // (TN_KCHUNK3_SHORT; A/B knob, default = kchunk3)
+      if (ps == 3 && sp.gemm.K <= 32 * c->shortk_max) ga.kchunk = c->kchunk3_short;
       ga.group_m = c->group_m;
       if (fused && sp.planes_consumer >= 0) ga.out_nplanes = passes[sp.planes_consumer] == 3 ? 4 : 2;
       Timer tm(c, 0, sp.tcc, sp.tmc, (int)s, sm);
@@ -2258,6 +2262,8 @@ tn_status tn_create(tn_ctx** out, int device, const tn_allocator* allocator, voi
   if (allocator) { c->alloc = *allocator; c->has_alloc = true; }
   c->num_sms = prop.multiProcessorCount;
   c->kchunk3 = env_int("TN_KCHUNK3", 1);
+  c->kchunk3_short = env_int("TN_KCHUNK3_SHORT", c->kchunk3);
+  c->shortk_max = env_int("TN_SHORTK_MAX", 16);
   // 1-pass: whole K in TMEM (promoting every 4 k-blocks costs 10 % and only moves the
   // all-1-pass C4 error from 2.9e-3 to 2.3e-3: fp16 operand rounding dominates there)
   c->kchunk1 = env_int("TN_KCHUNK1", 0);

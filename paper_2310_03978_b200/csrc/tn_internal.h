@@ -166,7 +166,7 @@ struct Knobs {
   int simt_old = 0;       // TN_SIMT_OLD: force the previous skinny design (A/B tests)
   int skinny_vec2 = 1;    // TN_SKINNY_VEC2=0: no paired-lane / k-pair 16-B accesses (tests)
   int gate_mma = 0;       // TN_GATE_MMA=1: gate-folded preps with K >= 4 on mma.sync (measured slower)
-  int l2hint = 1;         // TN_GEMM_L2HINT=0: operand TMA loads without the evict_last policy
+  int l2hint = 0;         // TN_GEMM_L2HINT=1: operand TMA loads with an evict_last policy (neutral)
   int narrow_mma = 1;     // TN_NARROW_MMA=0: N <= 64 GEMMs issue N = 128 MMAs (A/B tests)
   int prep_bp = 1;        // TN_PREP_BP=0: no bit-permutation transposer (A/B tests)
   int pair_min_m = 512;   // TN_GEMM_PAIR_MIN_M: CTA-pair GEMM from this M (0 = never)
