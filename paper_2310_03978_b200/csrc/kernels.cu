@@ -524,14 +524,6 @@ constexpr int GP_BUF = GP_TMAX + GP_TMAX / 32;     // X tile, then (aliased) the
 constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX / 8 * 8 /*dst*/ +
                            GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
 
-// Output tile position of destination element f: its 8-element vector q = f >> 3 keeps
-// its 64 B, the vector's four 16-B pairs rotated by (q >> 1) & 3, so the store phase's
-// eight lanes per 16-B access phase hit eight different bank groups.
-__device__ __forceinline__ int gp_swz(int f) {
-  const int q = f >> 3, e = f & 7;
-  return 8 * q + 2 * (((e >> 1) + (q >> 1)) & 3) + (e & 1);
-}
-
 // KT = K (gate inputs per output); a thread owns 16/KT carry positions, whose 16 X values
 // it keeps in registers, so the X tile's smem is reused for the outputs (4 blocks/SM)
 template <int PLANES, int KT>
@@ -620,18 +612,14 @@ __global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __res
           ai = fmaf(xs[i][k].x, y.y, fmaf(xs[i][k].y, y.x, ai));
         }
         const int f = fcp + s_fn[n];
-        buf[gp_swz(f)] = make_float2(ar, ai);
+        buf[f + (f >> 5)] = make_float2(ar, ai);
       }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
       float2 o[8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {   // 16-B reads of the swizzled pairs (conflict-free)
-        const float4 v = *reinterpret_cast<const float4*>(buf + 8 * q + 2 * ((c + (q >> 1)) & 3));
-        o[2 * c] = make_float2(v.x, v.y);
-        o[2 * c + 1] = make_float2(v.z, v.w);
-      }
+      for (int j = 0; j < 8; ++j) o[j] = buf[8 * q + j + ((8 * q) >> 5)];
       split_store8<PLANES>(d, dc + s_dst[q], o, scale);
     }
   }
@@ -1389,7 +1377,7 @@ __global__ void __launch_bounds__(128) einsum_wdotj_kernel(const EinsumDesc* __r
   };
   const int64_t units = d.J * NH;
   for (int64_t u_ = blockIdx.x * 4 + warp; u_ < units; u_ += (int64_t)gridDim.x * 4) {
-    const int64_t j = d.jperm ? (int64_t)d.jperm[u_ / NH] : u_ / NH;
+    const int64_t j = u_ / NH;
     const int n0 = (int)(u_ % NH) * NN;
     const int64_t ao = (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs;
     const int64_t bo = (d.ib ? (int64_t)d.ib[j] : 0) * d.b_gs;

@@ -66,7 +66,6 @@ struct StepPlan {
   double tcc = 0, tmc = 0;
   std::vector<int32_t> ia, ib;
   int64_t ia_off = -1, ib_off = -1;     // offsets into the device table buffer
-  int64_t jperm_off = -1;               // mode-4 merges: batch order (B-slab sorted)
   int64_t out_off = -1, out_elems = 0;  // arena element offset
   View out;
   // device descriptor indices
@@ -1300,15 +1299,6 @@ tn_status build_plan(tn_ctx* c) {
       sp.ib_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.ib.begin(), sp.ib.end());
     }
-    if (sp.merge && !sp.tc && sp.mode == 4 && sp.J > 1) {
-      // warp-per-batch merges: batches sorted by their B slab, so the warps of a block
-      // (and neighbouring blocks) read the same B slab at about the same time (L1 / L2)
-      std::vector<int32_t> perm((size_t)sp.J);
-      std::iota(perm.begin(), perm.end(), 0);
-      std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return sp.ib[a] < sp.ib[b]; });
-      sp.jperm_off = (int64_t)tables.size();
-      tables.insert(tables.end(), perm.begin(), perm.end());
-    }
     if (sp.dense_merge) {
       sp.pair_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.pair_map.begin(), sp.pair_map.end());
@@ -1622,7 +1612,6 @@ tn_status build_plan(tn_ctx* c) {
       e.J = sp.J;
       e.ia = sp.merge ? c->d_tables + sp.ia_off : nullptr;
       e.ib = sp.merge ? c->d_tables + sp.ib_off : nullptr;
-      e.jperm = (sp.jperm_off >= 0 && !c->host_only) ? c->d_tables + sp.jperm_off : nullptr;
       e.a_gs = gA.stride; e.b_gs = gB.stride;
       e.M = sp.m; e.N = sp.n; e.K = sp.k;
       e.nm = (int)FA.size(); e.nn = (int)FB.size(); e.nk = (int)K.size();

@@ -37,7 +37,6 @@ struct EinsumDesc {
   double* partial;                // mode 2: fp64 partial sums [2*J*M*N] (zeroed per launch)
   int64_t n_yslabs;               // mode 1 with J > 1: slabs of the small operand (all in smem)
   int64_t kchunk;                 // mode 2: k elements per block
-  const int32_t* jperm;           // mode 4: batches in B-slab order (nullable = 0..J-1)
 };
 
 // ---------------------------------------------------------------- operand prep
