@@ -423,13 +423,14 @@ def test_c3_sparse_state_sampled_subnetwork(ctx):
 
 
 @pytest.mark.timeout(900)
-def test_c4_sparse_state_sampled_subnetwork(ctx):
+@pytest.mark.parametrize("tag", ["a64", "a64b1"])
+def test_c4_sparse_state_sampled_subnetwork(ctx, tag):
     """Sycamore-53 m=18 with a 2^16-sample sparse-state boundary (the bench's
     `--boundary sparse16` order): one slice of a sub-network (extra bonds fixed) vs the
     oracle over all 2^16 amplitudes; the plan's dense slab-product merge (J ~ GA*GB)
     and gather-batched merges run at full width."""
     from tnworkloads.network import fix_bonds
-    w = configs.c4("sparse16")
+    w = configs.c4("sparse16", 32, tag)       # a64b1: the App. A.2 balanced order (DESIGN §5d)
     fine, pc = _refine(w, 2e11)
     extra = fine[len(w.sliced):]
     sub = fix_bonds(w.net, {x: 0 for x in extra})
@@ -441,7 +442,7 @@ def test_c4_sparse_state_sampled_subnetwork(ctx):
     c.close()
     ref = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
     err = rel_l2(got, ref)
-    print(f"C4 sparse16 sub-network: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
+    print(f"C4 sparse16 {tag} sub-network: extra bonds {len(extra)}, T_cc {pc.flops_per_slice:.3g}, "
           f"dense merges {sum(s['dense_merge'] for s in pj['steps'])}, rel_l2 {err:.3e}")
     assert err <= EXT_TOL
 
