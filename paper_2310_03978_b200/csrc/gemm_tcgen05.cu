@@ -260,14 +260,16 @@ __device__ __forceinline__ void tmem_wait_ld() {
 // half-filled sectors: the LSU, not DRAM, bounds output-heavy GEMMs).  Here the warp
 // writes 8 columns of its 32 rows into smem (row stride 10 float2: 16-B aligned,
 // conflict-free), then each store instruction writes 8 rows x 64 contiguous bytes.
-// base = element offset of this lane's row start (column n0); valid = the row exists.
+// base = element offset of this lane's row start (column n0); valid = the row exists;
+// ncols = columns to write (a multiple of 8, <= WC: narrow GEMMs write N < 64).
 template <int WC>
 __device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, const float* si,
                                                   float2* C, int64_t base, bool valid, int lane,
-                                                  float& amax, bool stream) {
+                                                  float& amax, bool stream, int ncols = WC) {
   const unsigned vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
   for (int i = 0; i < WC; i += 8) {
+    if (i >= ncols) break;
     float4* w = reinterpret_cast<float4*>(buf + lane * 10);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -288,6 +290,13 @@ __device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, 
     }
     __syncwarp();
   }
+}
+
+// 256-bit global store (STG.256: one full 32-B sector per lane)
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t* v) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 
 // shared-memory load through an explicit ld.shared (the column table is reached through a
@@ -733,6 +742,33 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
               }
               continue;
             }
+            if (args.planes_v16) {
+              // 16 plane-contiguous, 32-B aligned columns: one 256-bit store per plane, so
+              // every lane fills a whole sector (the 16-B vectors below fill half of one)
+#pragma unroll
+              for (int i = 0; i < WC; i += 16) {
+                if (n0 + i >= args.N) continue;
+                const int64_t a0 = rb + lds64(tc + i);
+                __align__(32) __half hr[16], hi[16], lr[16], li[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  const float xr = sr[i + jj] * ps, xi = si[i + jj] * ps;
+                  amax = fmaxf(amax, fmaxf(fabsf(sr[i + jj]), fabsf(si[i + jj])));
+                  plane_ovf |= fmaxf(fabsf(xr), fabsf(xi)) >= 65504.f;
+                  hr[jj] = __float2half_rn(xr);
+                  hi[jj] = __float2half_rn(xi);
+                  lr[jj] = __float2half_rn(xr - __half2float(hr[jj]));
+                  li[jj] = __float2half_rn(xi - __half2float(hi[jj]));
+                }
+                st_global_v8(P + a0, reinterpret_cast<const uint32_t*>(hr));
+                st_global_v8(P + pe + a0, reinterpret_cast<const uint32_t*>(hi));
+                if (args.out_nplanes == 4) {
+                  st_global_v8(P + 2 * pe + a0, reinterpret_cast<const uint32_t*>(lr));
+                  st_global_v8(P + 3 * pe + a0, reinterpret_cast<const uint32_t*>(li));
+                }
+              }
+              continue;
+            }
 #pragma unroll
             for (int i = 0; i < WC; i += 8) {
               if (n0 + i >= args.N) continue;
@@ -853,10 +889,11 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       }
       int64_t orow = (int64_t)j * args.M + m;
       if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
-      if (EW == 8 && !args.acc && (args.N % 2) == 0 && n0 + WC <= args.N) {
+      if (EW == 8 && !args.acc && (((args.N % 8) == 0 && n0 < args.N) || ((args.N % 2) == 0 && n0 + WC <= args.N))) {
+        // whole 8-column groups (narrow GEMMs: N = 8 .. 56 columns of the 64)
         store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C,
                               orow * (int64_t)args.N + n0, m < args.M && orow >= 0, lane, amax,
-                              args.l2hint != 0);
+                              args.l2hint != 0, min(WC, args.N - n0));
         continue;
       }
       if (m < args.M && n0 < args.N && orow >= 0) {

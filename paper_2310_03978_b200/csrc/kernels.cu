@@ -524,6 +524,11 @@ constexpr int GP_BUF = GP_TMAX + GP_TMAX / 32;     // X tile, then (aliased) the
 constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX / 8 * 8 /*dst*/ +
                            GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
 
+__device__ __forceinline__ bool g_regroup_ok(int on, int TD, int N, int KT, int CB) {
+  return on && TD == GP_TMAX && N % KT == 0 && CB % (16 / KT) == 0 &&
+         (N / KT) * (CB / (16 / KT)) == 256;
+}
+
 // KT = K (gate inputs per output); a thread owns 16/KT carry positions, whose 16 X values
 // it keeps in registers, so the X tile's smem is reused for the outputs (4 blocks/SM)
 template <int PLANES, int KT>
@@ -567,6 +572,9 @@ __global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __res
   }
   const bool vec = d.bp_vec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   constexpr int CPT = 16 / KT;                    // carry positions per thread
+  // regrouped compute (a full 4096-element tile, N a multiple of K): 256 threads x CPT
+  // carry positions x KT outputs; Ys rows 16-B aligned for the paired loads
+  const bool regroup = g_regroup_ok(d.g_regroup, TD, N, KT, CB);
   for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
     int64_t sc = 0, dc = 0;
     for (int i = 0; i < d.nc; ++i)
@@ -589,6 +597,62 @@ __global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __res
     }
     cp_async_wait_all();
     __syncthreads();
+    if (regroup) {
+      // thread = (n group nq of KT outputs, carry group cg of CPT positions cg + r*CGN): every
+      // Y row loaded (a warp-uniform broadcast) serves CPT outputs instead of one, and
+      // consecutive lanes read consecutive carry positions of X (conflict-free)
+      const int cgn = CB / CPT;
+      const int nq = threadIdx.x / cgn, cg = threadIdx.x - nq * cgn;
+      float2 xs[CPT][KT];
+#pragma unroll
+      for (int r = 0; r < CPT; ++r)
+#pragma unroll
+        for (int k = 0; k < KT; ++k) xs[r][k] = buf[cg + r * cgn + k * CB];
+      __syncthreads();   // X tile read into registers: buf becomes the output tile
+      // carry offsets cached in registers when each is reused KT >= 4 times (K <= 2: CPT >= 8
+      // positions would not fit the 64-register budget next to the X values)
+      constexpr bool FCR = KT >= 4;
+      int fcs[FCR ? CPT : 1];
+      if constexpr (FCR) {
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) fcs[r] = s_fc[cg + r * cgn];
+      }
+#pragma unroll
+      for (int jn = 0; jn < KT; ++jn) {
+        const int n = nq * KT + jn;
+        float2 y[KT];
+        if constexpr (KT % 2 == 0) {
+#pragma unroll
+          for (int k = 0; k < KT; k += 2) {
+            const float4 v = reinterpret_cast<const float4*>(Ys + n * KT)[k / 2];
+            y[k] = make_float2(v.x, v.y);
+            y[k + 1] = make_float2(v.z, v.w);
+          }
+        } else {
+          y[0] = Ys[n];
+        }
+        const int fn = s_fn[n];
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) {
+          float ar = 0.f, ai = 0.f;
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            ar = fmaf(xs[r][k].x, y[k].x, fmaf(-xs[r][k].y, y[k].y, ar));
+            ai = fmaf(xs[r][k].x, y[k].y, fmaf(xs[r][k].y, y[k].x, ai));
+          }
+          const int f = (FCR ? fcs[FCR ? r : 0] : (int)s_fc[cg + r * cgn]) + fn;
+          buf[f + (f >> 5)] = make_float2(ar, ai);
+        }
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
+        float2 o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = buf[8 * q + j + ((8 * q) >> 5)];
+        split_store8<PLANES>(d, dc + s_dst[q], o, scale);
+      }
+      continue;
+    }
     float2 xs[CPT][KT];
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
@@ -1434,6 +1498,117 @@ __global__ void __launch_bounds__(128) einsum_wdotj_kernel(const EinsumDesc* __r
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// Slab-staged variant of the warp dot (mode 4 variant 3, EinsumDesc.wd_*): the final
+// merges of the sparse boundary share each B slab between many batches while B's k order
+// is scattered (lanes over k would read 8 B per 32-B sector, 4x the bytes, once per
+// batch).  A block takes one contiguous part of one B slab — all k of N >> wd_t columns —
+// reads it once with coalesced loads into shared memory in [n_local][k] order (scatter
+// through two bit tables), then its warps run every batch of that slab: lanes over k, A
+// rows from global memory (per-k offsets from a smem table), B from smem without bank
+// conflicts, fp32 lane sums and an fp64 warp reduction per output (as einsum_wdotj).
+constexpr int WDS_WARPS = 16;
+constexpr int WDS_MAX_PART = 16384;   // elements of a staged part (128 KiB)
+__global__ void __launch_bounds__(32 * WDS_WARPS) einsum_wdots_kernel(const EinsumDesc* __restrict__ gd,
+                                                                     const int64_t* __restrict__ leaf_off) {
+  constexpr int MM = 4, NN = 8;
+  __shared__ __align__(16) EinsumDesc d;
+  __shared__ int32_t tlo[128], thi[128];
+  __shared__ int64_t am[MM];
+  extern __shared__ __align__(16) uint8_t wds_smem[];
+  copy_desc_to_smem(&d, gd);
+  float2* sB = reinterpret_cast<float2*>(wds_smem);                 // [np][K]
+  int32_t* ka = reinterpret_cast<int32_t*>(sB + ((int64_t)1 << d.wd_lb));   // [K]
+  const float2* A = d.A + d.a_off + (d.a_leaf >= 0 ? leaf_off[d.a_leaf] : 0);
+  const float2* B = d.B + d.b_off + (d.b_leaf >= 0 ? leaf_off[d.b_leaf] : 0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lb = d.wd_lb, llo = lb < 7 ? lb : 7, lhi = lb - llo;
+  const int M = (int)d.M, N = (int)d.N, K = (int)d.K;
+  for (int x = tid; x < (1 << llo); x += blockDim.x) {
+    int v = 0;
+    for (int b = 0; b < llo; ++b) if ((x >> b) & 1) v += d.wd_contrib[b];
+    tlo[x] = v;
+  }
+  for (int x = tid; x < (1 << lhi); x += blockDim.x) {
+    int v = 0;
+    for (int b = 0; b < lhi; ++b) if ((x >> b) & 1) v += d.wd_contrib[llo + b];
+    thi[x] = v;
+  }
+  if (tid < MM) am[tid] = tid < M ? decompose(tid, d.nm, d.m_ext, d.m_sa) : 0;
+  for (int k = tid; k < K; k += blockDim.x) ka[k] = (int32_t)decompose_sh(k, d.nk, d.k_sh, d.k_sa);
+  __syncthreads();
+  const int T = 1 << d.wd_t, P = 1 << lb, NP = d.wd_np;
+  const int NG = (NP + NN - 1) / NN;
+  const int lomask = (1 << llo) - 1;
+  float amax = 0.f;
+  for (int64_t u = blockIdx.x; u < d.wd_nslabs * T; u += gridDim.x) {
+    const int64_t slab = u / T;
+    const int part = (int)(u % T);
+    const int j0 = d.wd_start[slab], j1 = d.wd_start[slab + 1];
+    if (j0 == j1) continue;                      // uniform over the block
+    const float2* src = B + slab * d.b_gs + (int64_t)part * P;
+    // every element of the part in flight at once (8-B LDGSTS into its scattered slot)
+    for (int o = tid; o < P; o += blockDim.x) cp_async8(sB + tlo[o & lomask] + thi[o >> llo], src + o);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int task = warp; task < (j1 - j0) * NG; task += WDS_WARPS) {
+      const int64_t j = d.wd_list[j0 + task / NG];
+      const int nb0 = (task % NG) * NN;
+      const float2* Aj = A + (d.ia ? (int64_t)d.ia[j] : 0) * d.a_gs;
+      float cr[MM][NN], ci[MM][NN];
+#pragma unroll
+      for (int m = 0; m < MM; ++m)
+#pragma unroll
+        for (int n = 0; n < NN; ++n) { cr[m][n] = 0.f; ci[m][n] = 0.f; }
+      for (int k0 = lane; k0 < K; k0 += 64) {
+        const bool two = k0 + 32 < K;
+        float2 a[2][MM], b[2][NN];
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+          const bool ok = uu == 0 || two;
+          const int k = k0 + 32 * uu;
+          const int32_t kaa = ok ? ka[k] : 0;
+#pragma unroll
+          for (int m = 0; m < MM; ++m)
+            a[uu][m] = (ok && m < M) ? __ldg(Aj + am[m] + kaa) : make_float2(0.f, 0.f);
+#pragma unroll
+          for (int n = 0; n < NN; ++n)
+            b[uu][n] = (ok && nb0 + n < NP) ? sB[(nb0 + n) * K + k] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu)
+#pragma unroll
+          for (int n = 0; n < NN; ++n)
+#pragma unroll
+            for (int m = 0; m < MM; ++m) {
+              cr[m][n] = fmaf(a[uu][m].x, b[uu][n].x, fmaf(-a[uu][m].y, b[uu][n].y, cr[m][n]));
+              ci[m][n] = fmaf(a[uu][m].x, b[uu][n].y, fmaf(a[uu][m].y, b[uu][n].x, ci[m][n]));
+            }
+      }
+      double orr = 0.0, oi = 0.0;
+#pragma unroll
+      for (int m = 0; m < MM; ++m)
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          if (m < M && nb0 + n < NP) {
+            double r = cr[m][n], i = ci[m][n];
+            for (int o = 16; o > 0; o >>= 1) {
+              r += __shfl_xor_sync(0xffffffffu, r, o);
+              i += __shfl_xor_sync(0xffffffffu, i, o);
+            }
+            if (lane == m * NN + n) { orr = r; oi = i; }
+          }
+        }
+      const int m = lane / NN, nl = nb0 + lane % NN;
+      if (m < M && nl < NP) {
+        const int64_t n = (int64_t)d.wd_ptop[part] + d.wd_nloc[nl];
+        store_out(d, (j * M + m) * N + n, orr, oi, amax);
+      }
+    }
+    __syncthreads();
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
 // Variant for operands whose unit stride is the output dim n: lane = (k group, n), so
 // each load instruction reads NL consecutive n of 32/NL k values; one fp32 partial per
 // lane, reduced across the k groups in fp64.
@@ -1770,8 +1945,9 @@ int einsum_variants(const EinsumDesc& h) {
   if (h.mode == 1) return h.J > 1 ? 1 : 4;   // 0 heuristic rows, 1 previous design, 2..3: R = 1, 2
                                              // (batched merges: the new design only)
   if (h.mode == 3) return 2;   // 0 new design, 1 previous design
-  if (h.mode == 4)             // 0 lanes over k, 1 lanes over (k group, n), 2 warps per batch
-    return h.M <= 4 ? 3 : 2;
+  if (h.mode == 4)             // 0 lanes over k, 1 lanes over (k group, n), 2 warps per batch,
+                               // 3 slab-staged warps per batch (when eligible)
+    return h.wd_ok ? 4 : (h.M <= 4 ? 3 : 2);
   return 1;
 }
 
@@ -1853,7 +2029,22 @@ cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& h, const i
     const int64_t rows = h.J * h.M;
     int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    if (variant == 2) {
+    if (variant == 3 && h.wd_ok) {
+      const size_t smem = sizeof(float2) * ((size_t)1 << h.wd_lb) + sizeof(int32_t) * (size_t)h.K;
+      if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(einsum_wdots_kernel), (int)smem)) return e;
+      int64_t nb = h.wd_nslabs << h.wd_t;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, einsum_wdots_kernel, 32 * WDS_WARPS, smem) != cudaSuccess ||
+          per_sm < 1)
+        per_sm = 1;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (nb > (int64_t)sms * per_sm) nb = (int64_t)sms * per_sm;
+      einsum_wdots_kernel<<<(unsigned)std::max<int64_t>(nb, 1), 32 * WDS_WARPS, smem, s>>>(d_desc, leaf_off);
+      return cudaGetLastError();
+    }
+    if (variant == 2 || variant == 3) {
       int64_t jb = (h.J * ((h.N + 7) / 8) + 3) / 4;
       if (jb > 148 * 24) jb = 148 * 24;
       einsum_wdotj_kernel<4, 8><<<(unsigned)std::max<int64_t>(jb, 1), 128, 0, s>>>(d_desc, leaf_off);

@@ -66,6 +66,7 @@ struct StepPlan {
   double tcc = 0, tmc = 0;
   std::vector<int32_t> ia, ib;
   int64_t ia_off = -1, ib_off = -1;     // offsets into the device table buffer
+  int64_t wd_start_off = -1, wd_list_off = -1, wd_nslabs = 0;   // mode 4: batches by B slab
   int64_t out_off = -1, out_elems = 0;  // arena element offset
   View out;
   // device descriptor indices
@@ -765,6 +766,84 @@ void fill_shifts(tn::EinsumDesc& e) {
   e.pow2 = ok ? 1 : 0;
 }
 
+// Slab-staged warp dot (mode 4 variant 3): eligible when B's n and k bits tile its slab
+// exactly (the offsets of one slab are a bit permutation of [0, N*K)) and the top bits of
+// the slab offset are n bits, so a part of 2^lb elements — all k of N >> t columns — is
+// one contiguous run that fits shared memory.  Fills the wd_* fields (wd_ok = 1) or
+// leaves wd_ok = 0.
+void plan_wd_staged(tn::EinsumDesc& e, int64_t nslabs) {
+  e.wd_ok = 0;
+  if (!e.pow2 || e.J <= 1 || e.M > 4 || e.N > 256 || e.K > 8192 || e.a_gs >= (int64_t(1) << 31)) return;
+  if (e.J < 4 * nslabs) return;   // staging pays only when several batches share a slab
+  const int64_t NK = e.N * e.K;
+  int L = 0;
+  while ((int64_t(1) << L) < NK) ++L;
+  if ((int64_t(1) << L) != NK || L > 30 || e.b_gs < NK) return;
+  // weight bit -> (is_n, canonical weight)
+  std::vector<int> isn(L, -1);
+  std::vector<int64_t> canon(L, 0);
+  auto add = [&](int64_t stride, int sh, int64_t cw, int n) {
+    for (int b = 0; b < sh; ++b) {
+      const int64_t w = stride << b;
+      if ((w & (w - 1)) != 0 || w >= NK) return false;
+      int q = 0;
+      while ((int64_t(1) << q) < w) ++q;
+      if (isn[q] >= 0) return false;
+      isn[q] = n;
+      canon[q] = cw << b;
+    }
+    return true;
+  };
+  int64_t cw = 1;
+  for (int i = e.nn - 1; i >= 0; --i) {
+    if (!add(e.n_sb[i], e.n_sh[i], cw, 1)) return;
+    cw *= e.n_ext[i];
+  }
+  cw = 1;
+  for (int i = e.nk - 1; i >= 0; --i) {
+    if (!add(e.k_sb[i], e.k_sh[i], cw, 0)) return;
+    cw *= e.k_ext[i];
+  }
+  for (int q = 0; q < L; ++q) if (isn[q] < 0) return;
+  // smallest t with a part of <= 16384 elements (128 KiB) whose top t bits are n bits
+  int t = 0;
+  while (L - t > 14) {
+    if (t >= 3 || isn[L - 1 - t] != 1) return;
+    ++t;
+  }
+  const int lb = L - t;
+  // local n bits: the non-top n bits ranked by canonical weight
+  std::vector<std::pair<int64_t, int>> nb;
+  for (int q = 0; q < lb; ++q) if (isn[q] == 1) nb.push_back({canon[q], q});
+  std::sort(nb.begin(), nb.end());
+  if (nb.size() > 5) return;   // <= 32 local columns
+  for (int q = 0; q < 16; ++q) e.wd_contrib[q] = 0;
+  for (int q = 0; q < lb; ++q) {
+    if (isn[q] == 0) e.wd_contrib[q] = (int32_t)canon[q];
+    else {
+      int r = 0;
+      while (nb[r].second != q) ++r;
+      e.wd_contrib[q] = (int32_t)((int64_t(1) << r) * e.K);
+    }
+  }
+  const int np = 1 << (int)nb.size();
+  for (int x = 0; x < 32; ++x) {
+    int64_t v = 0;
+    for (int r = 0; r < (int)nb.size(); ++r) if ((x >> r) & 1) v += nb[r].first;
+    e.wd_nloc[x] = x < np ? (int32_t)v : 0;
+  }
+  for (int p = 0; p < 8; ++p) {
+    int64_t v = 0;
+    for (int i = 0; i < t; ++i) if ((p >> i) & 1) v += canon[lb + i];
+    e.wd_ptop[p] = p < (1 << t) ? (int32_t)v : 0;
+  }
+  e.wd_t = t;
+  e.wd_lb = lb;
+  e.wd_np = np;
+  e.wd_nslabs = nslabs;
+  e.wd_ok = 1;
+}
+
 void contiguous_strides(std::vector<VDim>& d) {
   int64_t s = 1;
   for (int p = (int)d.size() - 1; p >= 0; --p) {
@@ -895,6 +974,9 @@ tn_status build_plan(tn_ctx* c) {
   const int pair_min_m = tn::g_knobs.pair_min_m;            // CTA-pair GEMM for M >= this
   const int out_layout = env_int("TN_OUT_LAYOUT", 1);      // 1: [P keep][Q keep][con] for TC steps
   const int fuse_planes = env_int("TN_FUSE_PLANES", 1);    // producer epilogue writes consumer planes
+  const int plane_v16 = env_int("TN_PLANE_V16", 1);       // 256-bit plane stores where 16 columns are contiguous
+  const int wd_staged = env_int("TN_WD_STAGED", 1);       // mode-4 merges: slab-staged warp dot where eligible
+  const int gate_regroup = env_int("TN_GATE_REGROUP", 1);  // gate-folded prep: regrouped compute phase
   const int dense_mode = env_int("TN_DENSE_MERGE", 1);     // 0 off, 1 cost rule, 2 always (tests)
   // skinny steps folded into TC preps; gates with K > 8 stay separate
   // (their gate-prep is slower than skinny kernel + transposer on C4)
@@ -1299,6 +1381,21 @@ tn_status build_plan(tn_ctx* c) {
       sp.ib_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.ib.begin(), sp.ib.end());
     }
+    if (sp.merge && !sp.tc && sp.mode == 4 && sp.J > 1) {
+      // batches grouped by their B slab (CSR), for the slab-staged warp-dot kernel
+      int32_t ns = 0;
+      for (int32_t v : sp.ib) ns = std::max(ns, v + 1);
+      std::vector<int32_t> start(ns + 1, 0), list(sp.ib.size());
+      for (int32_t v : sp.ib) start[v + 1]++;
+      for (int32_t q = 0; q < ns; ++q) start[q + 1] += start[q];
+      std::vector<int32_t> fill(start.begin(), start.end() - 1);
+      for (size_t jj = 0; jj < sp.ib.size(); ++jj) list[fill[sp.ib[jj]]++] = (int32_t)jj;
+      sp.wd_nslabs = ns;
+      sp.wd_start_off = (int64_t)tables.size();
+      tables.insert(tables.end(), start.begin(), start.end());
+      sp.wd_list_off = (int64_t)tables.size();
+      tables.insert(tables.end(), list.begin(), list.end());
+    }
     if (sp.dense_merge) {
       sp.pair_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.pair_map.begin(), sp.pair_map.end());
@@ -1627,7 +1724,24 @@ tn_status build_plan(tn_ctx* c) {
       }
       if (sp.mode == 4) e.mode = 4;
       fill_shifts(e);
+      if (e.mode == 4 && sp.wd_start_off >= 0 && wd_staged) plan_wd_staged(e, sp.wd_nslabs);
+      if (e.wd_ok) {
+        e.wd_start = c->host_only ? nullptr : c->d_tables + sp.wd_start_off;
+        e.wd_list = c->host_only ? nullptr : c->d_tables + sp.wd_list_off;
+      }
       sp.hdesc = e;
+      if (c->debug_plan) {
+        fprintf(stderr, "[tn] step %d simt mode %d J=%lld M=%lld N=%lld K=%lld a_gs=%lld b_gs=%lld wd=%d(t=%d lb=%d np=%d) m:",
+                s, e.mode, (long long)e.J, (long long)e.M, (long long)e.N, (long long)e.K, (long long)e.a_gs,
+                (long long)e.b_gs, e.wd_ok, e.wd_t, e.wd_lb, e.wd_np);
+        for (int d = 0; d < e.nm; ++d) fprintf(stderr, " %lldx%lld", (long long)e.m_ext[d], (long long)e.m_sa[d]);
+        fprintf(stderr, " | n:");
+        for (int d = 0; d < e.nn; ++d) fprintf(stderr, " %lldx%lld", (long long)e.n_ext[d], (long long)e.n_sb[d]);
+        fprintf(stderr, " | k:");
+        for (int d = 0; d < e.nk; ++d)
+          fprintf(stderr, " %lldx(%lld,%lld)", (long long)e.k_ext[d], (long long)e.k_sa[d], (long long)e.k_sb[d]);
+        fprintf(stderr, "\n");
+      }
     } else {
       // P operand = A side unless swapped; both share the canonical K order
       memset(&sp.gemm, 0, sizeof(sp.gemm));
@@ -1879,6 +1993,21 @@ tn_status build_plan(tn_ctx* c) {
         for (int q = 0; q < g.n_qo; ++q) { g.qo_sh[q] = (uint8_t)qo[q].first; g.qo_str[q] = qo[q].second; }
         g.cols_contig = 0;   // plane mode has its own 8-column vectors
         g.cols_stride = 0;
+        // 256-bit plane stores: 16 plane-contiguous columns whose offsets are 16-element
+        // (32-B) aligned (every other stride and the plane size multiples of 16)
+        {
+          bool v16 = cols && qo.back().first >= 4 && pp.gemm.N % 16 == 0 && pp.out_elems % 16 == 0;
+          for (auto& d : po) v16 = v16 && d.second % 16 == 0;
+          for (size_t q = 0; q + 1 < qo.size(); ++q) v16 = v16 && qo[q].second % 16 == 0;
+          g.planes_v16 = (v16 && plane_v16) ? 1 : 0;
+        }
+        if (c->debug_plan) {
+          fprintf(stderr, "[tn] step %d planes%s rows:", ps, g.planes_v16 ? " v16" : "");
+          for (auto& d : po) fprintf(stderr, " 2^%dx%lld", d.first, (long long)d.second);
+          fprintf(stderr, " | cols:");
+          for (auto& d : qo) fprintf(stderr, " 2^%dx%lld", d.first, (long long)d.second);
+          fprintf(stderr, "\n");
+        }
         int lk = 0;
         while ((int64_t(1) << lk) < pp.k) ++lk;
         g.plane_exp = -16 - lk;
@@ -1930,6 +2059,7 @@ tn_status build_plan(tn_ctx* c) {
         trial.gy = pp.hdesc.B;
         trial.gy_off = pp.hdesc.b_off;
         trial.gy_leaf = pp.hdesc.b_leaf;
+        trial.g_regroup = gate_regroup;
         if (!c->host_only) {
           trial.absmax_in = c->d_absmax + pp.x_slot;
           trial.absmax_y = c->d_absmax + pp.y_slot;
@@ -2038,7 +2168,7 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
       }
       // untuned (accumulating final steps are never re-run): batched merges with a tiny
       // per-batch output take the warp-per-batch kernel
-      int var = sp.simt_variant >= 0 ? sp.simt_variant : (sp.hdesc.mode == 4 && nv == 3 ? 2 : 0);
+      int var = sp.simt_variant >= 0 ? sp.simt_variant : (sp.hdesc.mode == 4 && nv >= 3 ? nv - 1 : 0);
       if (c->simt_force >= 0) var = std::min(c->simt_force, nv - 1);
       Timer tm(c, 2, sp.tcc, sp.tmc, (int)s, sm);
       TN_CUDA(tn::launch_einsum(c->d_einsum + sp.einsum_idx, sp.hdesc, c->d_leaf_off, sm, var));
@@ -2545,13 +2675,14 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"folded\":%s,\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"folded\":%s,\"wd_staged\":%s,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
              sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false",
              sp.tc ? (sp.skip_prep[0] ? -1 : sp.r_fast[0]) : -1,
              sp.tc ? (sp.skip_prep[1] ? -1 : sp.r_fast[1]) : -1, sp.planes_consumer >= 0 ? "true" : "false",
-             sp.dense_merge ? "true" : "false", sp.folded ? "true" : "false");
+             sp.dense_merge ? "true" : "false", sp.folded ? "true" : "false",
+             (!sp.tc && sp.hdesc.wd_ok) ? "true" : "false");
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";

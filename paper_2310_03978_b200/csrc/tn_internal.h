@@ -37,6 +37,17 @@ struct EinsumDesc {
   double* partial;                // mode 2: fp64 partial sums [2*J*M*N] (zeroed per launch)
   int64_t n_yslabs;               // mode 1 with J > 1: slabs of the small operand (all in smem)
   int64_t kchunk;                 // mode 2: k elements per block
+  // mode 4, slab-staged variant (wd_ok = 1): the batches are grouped by B slab (CSR
+  // wd_start[wd_nslabs + 1] / wd_list[J]); a block stages one contiguous part of a B slab
+  // (2^wd_lb elements: the top wd_t bits of the slab offset are n bits) into shared memory
+  // in [n_local][k] order, then its warps run that slab's batches with B from smem
+  const int32_t* wd_start; const int32_t* wd_list;
+  int64_t wd_nslabs;
+  int32_t wd_ok, wd_t, wd_lb, wd_np;
+  int32_t wd_contrib[16];         // part-offset bit b -> smem index weight (k: canonical k;
+                                  // n: (1 << local n bit) * K)
+  int32_t wd_nloc[32];            // local n index -> canonical output column
+  int32_t wd_ptop[8];             // part index -> canonical output column offset
 };
 
 // ---------------------------------------------------------------- operand prep
@@ -74,7 +85,7 @@ struct PrepDesc {
   // out[o][n][v] = sum_k Y[n][k] X[o, v, k] that is never materialised: src is X, the
   // tile holds X values (carry bits + k bits), each plane element applies Y on the fly.
   // bp_tab: [src lo/hi 128][dst T/8][cn: T int32 (carry pos | n << 16)]
-  const float2* gy; int64_t gy_off; int32_t gy_leaf, g_N, g_K, g_cbits, g_ts, g_nn, g_nk, pad_g;
+  const float2* gy; int64_t gy_off; int32_t gy_leaf, g_N, g_K, g_cbits, g_ts, g_nn, g_nk, g_regroup;   // g_regroup: 1 = regrouped compute
   int64_t gy_n_ext[8], gy_n_s[8], gy_k_ext[8], gy_k_s[8];
   const unsigned* absmax_y;
   __half* dst; int64_t plane_elems;
@@ -139,6 +150,8 @@ struct GemmArgs {
   const int32_t* pair_map;
   int32_t pm_sh_m, pm_sh_n, pm_g1;
   int32_t narrow;                 // N <= 64: N = 64 MMA instructions (one column tile)
+  int32_t planes_v16;             // plane mode, columns: 16 plane-contiguous columns, 32-B
+                                  // aligned -> one 256-bit store per plane and 16 columns
 };
 
 // ---------------------------------------------------------------- slice select
