@@ -258,36 +258,49 @@ __device__ __forceinline__ void tmem_wait_ld() {
 // Row-contiguous output through a per-warp smem stage.  The TMEM layout gives each
 // lane one row, so a direct store instruction touches 32 rows with 16 B each (32
 // half-filled sectors: the LSU, not DRAM, bounds output-heavy GEMMs).  Here the warp
-// writes 8 columns of its 32 rows into smem (row stride 10 float2: 16-B aligned,
-// conflict-free), then each store instruction writes 8 rows x 64 contiguous bytes.
+// writes 8 columns of its 32 rows into smem (64-B rows, 16-B units XOR-swizzled by
+// bits 1-2 of the row: conflict-free both ways), then each store instruction writes
+// 8 rows x 64 contiguous bytes.  The four row bases a lane stores to are fetched once
+// (not per column group), the four reads of a group are issued before its stores, and
+// padding rows are masked by predicated stores (no divergent branch per store).
 // base = element offset of this lane's row start (column n0); valid = the row exists;
 // ncols = columns to write (a multiple of 8, <= WC: narrow GEMMs write N < 64).
+__device__ __forceinline__ void st_global_v4_pred(void* p, float4 v, bool ok) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %5, 0;\n@q st.global.v4.f32 [%0], {%1,%2,%3,%4};\n}" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((int)ok)
+               : "memory");
+}
 template <int WC>
-__device__ __forceinline__ void store_rows_staged(float2* buf, const float* sr, const float* si,
+__device__ __forceinline__ void store_rows_staged(float4* buf, const float* sr, const float* si,
                                                   float2* C, int64_t base, bool valid, int lane,
-                                                  float& amax, bool stream, int ncols = WC) {
+                                                  float& amax, int ncols = WC) {
   const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  const int c = lane & 3;
+  float2* rowp[4];
+  bool ok[4];
+  int slot[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = (lane >> 2) + 8 * q;
+    rowp[q] = C + __shfl_sync(0xffffffffu, base, r) + 2 * c;
+    ok[q] = (vmask >> r) & 1u;
+    slot[q] = r * 4 + (c ^ ((r >> 1) & 3));
+  }
 #pragma unroll
   for (int i = 0; i < WC; i += 8) {
     if (i >= ncols) break;
-    float4* w = reinterpret_cast<float4*>(buf + lane * 10);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float r0 = sr[i + 2 * c], i0 = si[i + 2 * c], r1 = sr[i + 2 * c + 1], i1 = si[i + 2 * c + 1];
-      w[c] = make_float4(r0, i0, r1, i1);
+    for (int cc = 0; cc < 4; ++cc) {
+      const float r0 = sr[i + 2 * cc], i0 = si[i + 2 * cc], r1 = sr[i + 2 * cc + 1], i1 = si[i + 2 * cc + 1];
+      buf[lane * 4 + (cc ^ ((lane >> 1) & 3))] = make_float4(r0, i0, r1, i1);
       if (valid) amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r0), fabsf(i0)), fmaxf(fabsf(r1), fabsf(i1))));
     }
     __syncwarp();
+    float4 v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = (lane >> 2) + 8 * q, c = lane & 3;
-      const int64_t rb = __shfl_sync(0xffffffffu, base, r);
-      const float4 v = reinterpret_cast<const float4*>(buf + r * 10)[c];
-      if ((vmask >> r) & 1u) {
-        if (stream) __stcs(reinterpret_cast<float4*>(C + rb + i + 2 * c), v);   // evict-first
-        else *reinterpret_cast<float4*>(C + rb + i + 2 * c) = v;
-      }
-    }
+    for (int q = 0; q < 4; ++q) v[q] = buf[slot[q]];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st_global_v4_pred(rowp[q] + i, v[q], ok[q]);
     __syncwarp();
   }
 }
@@ -803,8 +816,8 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
             t >>= sh;
           }
           const int64_t rb = (int64_t)j * args.M * (int64_t)args.N + moff + lds64(tab + colh * WC);
-          store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C, rb, m < args.M,
-                                lane, amax, args.l2hint != 0);
+          store_rows_staged<WC>(reinterpret_cast<float4*>(stage_buf + (warp - EPI_WARP0) * 32 * 10), sr, si,
+                                args.C, rb, m < args.M, lane, amax);
           continue;
         }
         if (m < args.M && n0 < args.N) {
@@ -891,9 +904,9 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
       if (args.rowmap && m < args.M) orow = args.rowmap[m];   // grouped merge: -1 = padding row
       if (EW == 8 && !args.acc && (((args.N % 8) == 0 && n0 < args.N) || ((args.N % 2) == 0 && n0 + WC <= args.N))) {
         // whole 8-column groups (narrow GEMMs: N = 8 .. 56 columns of the 64)
-        store_rows_staged<WC>(stage_buf + (warp - EPI_WARP0) * 32 * 10, sr, si, args.C,
-                              orow * (int64_t)args.N + n0, m < args.M && orow >= 0, lane, amax,
-                              args.l2hint != 0, min(WC, args.N - n0));
+        store_rows_staged<WC>(reinterpret_cast<float4*>(stage_buf + (warp - EPI_WARP0) * 32 * 10), sr, si,
+                              args.C, orow * (int64_t)args.N + n0, m < args.M && orow >= 0, lane, amax,
+                              min(WC, args.N - n0));
         continue;
       }
       if (m < args.M && n0 < args.N && orow >= 0) {

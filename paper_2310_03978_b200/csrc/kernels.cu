@@ -438,6 +438,35 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Outer tile offsets Σ_{bit i of c} (c_src[i], c_dst[i]) without a per-thread loop over
+// the descriptor: lane i holds bit i's pair in registers (loaded once), the warp sums the
+// set bits with a butterfly (every lane ends with the totals).  nc > 32: the plain loop.
+struct TileBits {
+  int64_t s0, d0;
+};
+__device__ __forceinline__ TileBits tile_bits_load(const int64_t* c_src, const int64_t* c_dst, int nc, int lane) {
+  return TileBits{lane < nc ? c_src[lane] : 0, lane < nc ? c_dst[lane] : 0};
+}
+__device__ __forceinline__ void tile_bits_sum(const TileBits& t, uint64_t c, int lane, int nc, const int64_t* c_src,
+                                              const int64_t* c_dst, int64_t& sc, int64_t& dc) {
+  if (nc > 32) {
+    sc = 0;
+    dc = 0;
+    for (int i = 0; i < nc; ++i)
+      if ((c >> i) & 1) { sc += c_src[i]; dc += c_dst[i]; }
+    return;
+  }
+  const bool b = (c >> lane) & 1u;
+  int64_t s = b ? t.s0 : 0, d = b ? t.d0 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+  }
+  sc = s;
+  dc = d;
+}
+
 constexpr int BP_TMAX = 4096;
 constexpr size_t BP_SMEM = BP_TMAX * 8 + BP_TMAX / 8 * 8 + 128 * 8 + BP_TMAX * 2 + BP_TMAX / 16;
 
@@ -469,12 +498,14 @@ __global__ void __launch_bounds__(256, 4) prep_bp_kernel(const PrepDesc* __restr
   const bool vec = d.bp_vec && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   const int64_t tiles = d.G * d.nC;
   const int64_t rk = d.R * d.Kpad;
+  const TileBits tb = tile_bits_load(d.c_src, d.c_dst, d.nc, threadIdx.x & 31);
   for (int64_t c = blockIdx.x; c < tiles; c += gridDim.x) {
     const int64_t g = c >> d.nc;                     // nC = 2^nc tiles per slab
     const int64_t cc = c - (g << d.nc);
-    int64_t sc = g * d.g_stride, dc = g * rk;
-    for (int i = 0; i < d.nc; ++i)
-      if ((cc >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
+    int64_t sc, dc;
+    tile_bits_sum(tb, (uint64_t)cc, threadIdx.x & 31, d.nc, d.c_src, d.c_dst, sc, dc);
+    sc += g * d.g_stride;
+    dc += g * rk;
     __syncthreads();   // tables ready / previous tile consumed
     const float2* sp = src + sc;
     // every load of the tile in flight at once, straight to shared memory (LDGSTS)
@@ -523,6 +554,14 @@ constexpr int GP_YMAX = 512, GP_NMAX = 256;
 constexpr int GP_BUF = GP_TMAX + GP_TMAX / 32;     // X tile, then (aliased) the padded output tile
 constexpr size_t GP_SMEM = GP_BUF * 8 + GP_YMAX * 8 + 128 * 8 /*src*/ + GP_TMAX / 8 * 8 /*dst*/ +
                            GP_TMAX * 2 /*fc*/ + GP_NMAX * 2 /*fn*/;
+
+// output tile slot of destination-order element f: 16-B pairs (f >> 1) XOR-swizzled inside
+// their 128-B row by bits 3-5 of the pair index, so the 8 lanes of a 128-bit read phase
+// (pairs 4q + t, q = q0 .. q0 + 7) hit 8 different bank groups
+__device__ __forceinline__ int gp_swz(int f) {
+  const int u = f >> 1;
+  return ((u ^ ((u >> 3) & 7)) << 1) | (f & 1);
+}
 
 __device__ __forceinline__ bool g_regroup_ok(int on, int TD, int N, int KT, int CB) {
   return on && TD == GP_TMAX && N % KT == 0 && CB % (16 / KT) == 0 &&
@@ -575,10 +614,10 @@ __global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __res
   // regrouped compute (a full 4096-element tile, N a multiple of K): 256 threads x CPT
   // carry positions x KT outputs; Ys rows 16-B aligned for the paired loads
   const bool regroup = g_regroup_ok(d.g_regroup, TD, N, KT, CB);
+  const TileBits tb = tile_bits_load(d.c_src, d.c_dst, d.nc, threadIdx.x & 31);
   for (int64_t c = blockIdx.x; c < d.nC; c += gridDim.x) {
-    int64_t sc = 0, dc = 0;
-    for (int i = 0; i < d.nc; ++i)
-      if ((c >> i) & 1) { sc += d.c_src[i]; dc += d.c_dst[i]; }
+    int64_t sc, dc;
+    tile_bits_sum(tb, (uint64_t)c, threadIdx.x & 31, d.nc, d.c_src, d.c_dst, sc, dc);
     __syncthreads();   // tables / Y ready, previous tile's outputs consumed
     const float2* sp = src + sc;
     // every load of the tile in flight at once, straight to shared memory (LDGSTS)
@@ -641,14 +680,18 @@ __global__ void __launch_bounds__(256, 4) prep_gate_kernel(const PrepDesc* __res
             ai = fmaf(xs[r][k].x, y[k].y, fmaf(xs[r][k].y, y[k].x, ai));
           }
           const int f = (FCR ? fcs[FCR ? r : 0] : (int)s_fc[cg + r * cgn]) + fn;
-          buf[f + (f >> 5)] = make_float2(ar, ai);
+          buf[gp_swz(f)] = make_float2(ar, ai);
         }
       }
       __syncthreads();
       for (int q = threadIdx.x; q < TD / 8; q += blockDim.x) {
         float2 o[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = buf[8 * q + j + ((8 * q) >> 5)];
+        for (int j = 0; j < 8; j += 2) {   // 16-B pairs, conflict-free under the swizzle
+          const float4 v = reinterpret_cast<const float4*>(buf)[gp_swz(8 * q + j) >> 1];
+          o[j] = make_float2(v.x, v.y);
+          o[j + 1] = make_float2(v.z, v.w);
+        }
         split_store8<PLANES>(d, dc + s_dst[q], o, scale);
       }
       continue;
