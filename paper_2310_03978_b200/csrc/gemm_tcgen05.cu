@@ -609,7 +609,11 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
     const int row = quad * 32 + lane;
     // the operands carry 2^sA and 2^sB (|s| <= 120 each): 2^-(sA+sB) may leave the fp32
     // range, so 2^-sA is folded into the chunk promotion and 2^-sB applied once per tile
-    const float scale = ldexpf(1.0f, -*args.scaleA);
+    // both exponents folded into the chunk scale when 2^-(sA+sB) is a normal fp32 (the
+    // final per-tile multiply is then skipped)
+    const int sab_all = *args.scaleA + *args.scaleB;
+    const bool fold_ab = sab_all >= -100 && sab_all <= 100;
+    const float scale = ldexpf(1.0f, fold_ab ? -sab_all : -*args.scaleA);
     const float scale_b = ldexpf(1.0f, -*args.scaleB);
     // fused plane output: consumer exponent sC = max(bound, delayed scaling); the planes
     // hold x * 2^sC = acc * 2^(sC - sA - sB)
@@ -665,6 +669,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
         if (cols_live) {
 #pragma unroll
           for (int c = 0; c < WC / 32; ++c) {
+            if (c > 0 && nt * BN + colh * WC + c * 32 >= args.N) break;   // narrow: dead 32-column group
             uint32_t vr[32], vi[32];
             TN_LD32(vr, tb + c * 32);
             TN_LD32(vi, tb + im_off + c * 32);
@@ -687,8 +692,10 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
         if (args.narrow) eb ^= 1;
         else cb ^= 1;
       }
+      if (!fold_ab) {
 #pragma unroll
-      for (int i = 0; i < WC; ++i) { sr[i] *= scale_b; si[i] *= scale_b; }
+        for (int i = 0; i < WC; ++i) { sr[i] *= scale_b; si[i] *= scale_b; }
+      }
       int m = mt * C::TILE_M + (int)rank * BM + row;
       const int n0 = nt * BN + colh * WC;
       if (args.out_gen) {
@@ -725,6 +732,7 @@ __global__ void __launch_bounds__(32 * EPI_WARP0 + 32 * EW, 1) cgemm_tcgen05_ker
               const int64_t gb = __shfl_sync(0xffffffffu, rb, 8 * g);
 #pragma unroll
               for (int i = 0; i < WC; i += 8) {
+                if (n0 + i >= args.N) break;         // warp-uniform: narrow tiles stop early
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                   buf[lane * 9 + jj] = make_float2(sr[i + jj] * ps, si[i + jj] * ps);

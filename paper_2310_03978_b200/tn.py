@@ -92,6 +92,10 @@ def lib():
     if _lib is not None:
         return _lib
     from . import _build
+    alt = os.environ.get("TN_LIB_PATH")      # tooling only: A/B of two builds (tools/gpu_ab.sh)
+    if alt:
+        _lib = _bind(C.CDLL(alt))
+        return _lib
     if _build.needs_build():
         have_nvcc = os.path.exists(_build.NVCC)
         if have_nvcc:
@@ -101,7 +105,12 @@ def lib():
                 raise TNLibraryError(f"libtn.so could not be built: {e}") from e
         elif not os.path.exists(LIB_PATH):
             raise TNLibraryError(f"libtn.so missing and nvcc not found at {_build.NVCC}")
-    L = C.CDLL(LIB_PATH)
+    _lib = _bind(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def _bind(L):
+    """Declare the C-ABI signatures (include/tn.h) on a loaded libtn."""
     P, I32, I64, D, VP = C.POINTER, C.c_int32, C.c_int64, C.c_double, C.c_void_p
     sig = {
         "tn_create": [P(VP), C.c_int, P(Allocator), VP],
@@ -131,7 +140,6 @@ def lib():
     L.tn_version.restype = C.c_char_p
     L.tn_destroy.argtypes = [VP]
     L.tn_destroy.restype = None
-    _lib = L
     return L
 
 

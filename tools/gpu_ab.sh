@@ -10,5 +10,6 @@ P="tools/step_profile.py --workload c4 --boundary ${BOUNDARY:-sparse16} --peak 3
 timeout 600 python $P --out gpurun_out/steps_A.json > gpurun_out/steps_A.txt 2>&1
 env $AB_ENV_B timeout 600 python $P --out gpurun_out/steps_B.json > gpurun_out/steps_B.txt 2>&1
 timeout 600 python $P --out gpurun_out/steps_A2.json > gpurun_out/steps_A2.txt 2>&1
-head -1 gpurun_out/steps_A.txt gpurun_out/steps_B.txt gpurun_out/steps_A2.txt
-python tools/ab_compare.py ms | head -30
+env $AB_ENV_B timeout 600 python $P --out gpurun_out/steps_B2.json > gpurun_out/steps_B2.txt 2>&1
+head -1 gpurun_out/steps_A.txt gpurun_out/steps_B.txt gpurun_out/steps_A2.txt gpurun_out/steps_B2.txt
+python tools/ab_compare.py ms 2>/dev/null | head -30
