@@ -1652,6 +1652,143 @@ __global__ void __launch_bounds__(32 * WDS_WARPS) einsum_wdots_kernel(const Eins
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
+// ---------------------------------------------------------------- fused skinny chain
+// tn::ChainDesc (tn_internal.h).  A block takes a tile of 32 carry positions
+// (lane = carry position: unit stride in the chain's input T0 and output TL), loads T0's
+// touched elements into smem W0[e][lane], runs the steps W_{i-1} -> W_i in smem (warp task =
+// one o-position p and up to 8 outputs n: the K inputs of p in registers, Y rows broadcast
+// from smem, the same fp32 k-ordered sums as einsum_skinny_kernel) and stores W_L.
+constexpr int CH_THREADS = 256;
+
+// one chain step W_{i-1} -> W_i for K inputs and NG outputs per warp task (templated so the
+// k loop and the NG output chains unroll: NG independent FMA chains per task)
+template <int K, int NG>
+__device__ __forceinline__ void chain_step(const float2* __restrict__ W, float2* __restrict__ O,
+                                           const float2* __restrict__ Ys, const int32_t* in_p,
+                                           const int32_t* out_p, const int32_t* in_k, const int32_t* out_n,
+                                           int P, int N, int warp, int lane) {
+  const int ngr = N / NG;
+  for (int task = warp; task < P * ngr; task += CH_THREADS / 32) {
+    const int p = task / ngr, nb = (task - p * ngr) * NG;
+    float2 x[K];
+    const int ip = in_p[p];
+#pragma unroll
+    for (int k = 0; k < K; ++k) x[k] = W[(ip + in_k[k]) * 32 + lane];
+    const int op = out_p[p];
+    float ar[NG], ai[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) { ar[j] = 0.f; ai[j] = 0.f; }
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        const float2* y = Ys + (nb + j) * K + k;
+        float2 b0, b1 = make_float2(0.f, 0.f);
+        if constexpr (K >= 2) {
+          const float4 q = *reinterpret_cast<const float4*>(y);   // broadcast 16-B pair
+          b0 = make_float2(q.x, q.y);
+          b1 = make_float2(q.z, q.w);
+        } else {
+          b0 = y[0];
+        }
+        ar[j] = fmaf(x[k].x, b0.x, fmaf(-x[k].y, b0.y, ar[j]));
+        ai[j] = fmaf(x[k].x, b0.y, fmaf(x[k].y, b0.x, ai[j]));
+        if constexpr (K >= 2) {
+          ar[j] = fmaf(x[k + 1].x, b1.x, fmaf(-x[k + 1].y, b1.y, ar[j]));
+          ai[j] = fmaf(x[k + 1].x, b1.y, fmaf(x[k + 1].y, b1.x, ai[j]));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) O[(op + out_n[nb + j]) * 32 + lane] = make_float2(ar[j], ai[j]);
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void chain_step_k(const float2* W, float2* O, const float2* Ys, const int32_t* in_p,
+                                             const int32_t* out_p, const int32_t* in_k, const int32_t* out_n,
+                                             int P, int N, int warp, int lane) {
+  if (N >= 8) chain_step<K, 8>(W, O, Ys, in_p, out_p, in_k, out_n, P, N, warp, lane);
+  else if (N == 4) chain_step<K, 4>(W, O, Ys, in_p, out_p, in_k, out_n, P, N, warp, lane);
+  else if (N == 2) chain_step<K, 2>(W, O, Ys, in_p, out_p, in_k, out_n, P, N, warp, lane);
+  else chain_step<K, 1>(W, O, Ys, in_p, out_p, in_k, out_n, P, N, warp, lane);
+}
+
+__global__ void __launch_bounds__(CH_THREADS) einsum_chain_kernel(const ChainDesc* __restrict__ gd,
+                                                                 const int64_t* __restrict__ leaf_off) {
+  __shared__ __align__(16) ChainDesc d;
+  copy_desc_to_smem(&d, gd);
+  extern __shared__ __align__(16) uint8_t ch_smem[];
+  float2* bufA = reinterpret_cast<float2*>(ch_smem);
+  float2* bufB = bufA + 32 * (size_t)d.buf_a;
+  float2* Ys = bufB + 32 * (size_t)d.buf_b;
+  int ysz = 0;
+  for (int i = 0; i < d.L; ++i) ysz += (d.st[i].N * d.st[i].K + 1) & ~1;
+  int32_t* tab = reinterpret_cast<int32_t*>(Ys + ysz);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < d.n_tab; i += CH_THREADS) tab[i] = d.tab[i];
+  __syncthreads();
+  {
+    int yo = 0;
+    for (int i = 0; i < d.L; ++i) {
+      const ChainStep& st = d.st[i];
+      const float2* Y = st.Y + st.y_off + (st.y_leaf >= 0 ? leaf_off[st.y_leaf] : 0);
+      const int32_t* yoff = tab + st.tab + 2 * st.P + st.K + st.N;
+      for (int e = tid; e < st.N * st.K; e += CH_THREADS) Ys[yo + e] = Y[yoff[e]];
+      yo += (st.N * st.K + 1) & ~1;      // 16-B aligned regions (paired Y loads)
+    }
+  }
+  const float2* src = d.src + d.src_off + (d.src_leaf >= 0 ? leaf_off[d.src_leaf] : 0);
+  const TileBits tb = tile_bits_load(d.ct_src, d.ct_dst, d.nct, lane);
+  int64_t ls = 0, ld = 0;                      // this lane's carry offsets in T0 / TL
+#pragma unroll
+  for (int b = 0; b < 5; ++b)
+    if ((lane >> b) & 1) { ls += d.lw_src[b]; ld += d.lw_dst[b]; }
+  const int n0 = 1 << d.a0, nL = 1 << d.aL;
+  const int32_t* t0off = tab;
+  const int32_t* tLoff = tab + n0;
+  float amax = 0.f;
+  for (int64_t t = blockIdx.x; t < d.n_tiles; t += gridDim.x) {
+    int64_t cs, cdst;
+    tile_bits_sum(tb, (uint64_t)t, lane, d.nct, d.ct_src, d.ct_dst, cs, cdst);
+    __syncthreads();                 // Y staged / previous tile's W_L stored
+    const float2* sp = src + cs + ls;
+    // every load of the tile in flight at once (8-B LDGSTS straight into W0)
+    for (int e = warp; e < n0; e += CH_THREADS / 32) cp_async8(bufA + e * 32 + lane, sp + t0off[e]);
+    cp_async_wait_all();
+    __syncthreads();
+    int yo = 0;
+    for (int i = 0; i < d.L; ++i) {
+      const ChainStep& st = d.st[i];
+      const float2* W = st.in_buf ? bufB : bufA;
+      float2* O = st.in_buf ? bufA : bufB;
+      const int32_t* in_p = tab + st.tab;
+      const int32_t* out_p = in_p + st.P;
+      const int32_t* in_k = out_p + st.P;
+      const int32_t* out_n = in_k + st.K;
+      const int K = st.K, N = st.N;
+      const float2* Yst = Ys + yo;
+      switch (K) {   // the planner admits K = 1, 2, 4, 8, 16 (powers of two <= 16)
+        case 1: chain_step_k<1>(W, O, Yst, in_p, out_p, in_k, out_n, st.P, N, warp, lane); break;
+        case 2: chain_step_k<2>(W, O, Yst, in_p, out_p, in_k, out_n, st.P, N, warp, lane); break;
+        case 4: chain_step_k<4>(W, O, Yst, in_p, out_p, in_k, out_n, st.P, N, warp, lane); break;
+        case 8: chain_step_k<8>(W, O, Yst, in_p, out_p, in_k, out_n, st.P, N, warp, lane); break;
+        default: chain_step_k<16>(W, O, Yst, in_p, out_p, in_k, out_n, st.P, N, warp, lane); break;
+      }
+      yo += (N * K + 1) & ~1;
+      __syncthreads();
+    }
+    const float2* WL = (d.L & 1) ? bufB : bufA;
+    float2* dp = d.dst + cdst + ld;
+    for (int e = warp; e < nL; e += CH_THREADS / 32) {
+      const float2 v = WL[e * 32 + lane];
+      dp[tLoff[e]] = v;
+      amax = fmaxf(amax, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+  }
+  if (d.absmax_out) block_absmax(amax, d.absmax_out);
+}
+
 // Variant for operands whose unit stride is the output dim n: lane = (k group, n), so
 // each load instruction reads NL consecutive n of 32/NL k values; one fp32 partial per
 // lane, reduced across the k groups in fp64.
@@ -1982,6 +2119,27 @@ void launch_wide(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* l
   if (vec2) einsum_wide_kernel<KMAX, 2, 1><<<grid_for(h.M / 2, 256), 256, smem, s>>>(d_desc, leaf_off);
   else if (kpair) einsum_wide_kernel<KMAX, 1, 2><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
   else einsum_wide_kernel<KMAX, 1, 1><<<grid_for(h.M, 256), 256, smem, s>>>(d_desc, leaf_off);
+}
+
+size_t chain_smem_bytes(const ChainDesc& d) {
+  size_t ys = 0;
+  for (int i = 0; i < d.L; ++i) ys += ((size_t)d.st[i].N * d.st[i].K + 1) & ~(size_t)1;
+  return sizeof(float2) * (32 * ((size_t)d.buf_a + d.buf_b) + ys) + sizeof(int32_t) * (size_t)d.n_tab;
+}
+
+cudaError_t launch_chain(const ChainDesc* d_desc, const ChainDesc& h, const int64_t* leaf_off, cudaStream_t s) {
+  const size_t smem = chain_smem_bytes(h);
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(einsum_chain_kernel), (int)smem)) return e;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, einsum_chain_kernel, CH_THREADS, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t g = std::min<int64_t>(h.n_tiles, (int64_t)sms * per_sm);
+  einsum_chain_kernel<<<(unsigned)std::max<int64_t>(g, 1), CH_THREADS, smem, s>>>(d_desc, leaf_off);
+  return cudaGetLastError();
 }
 
 int einsum_variants(const EinsumDesc& h) {

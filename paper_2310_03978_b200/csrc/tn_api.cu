@@ -95,6 +95,11 @@ struct StepPlan {
   // its tensor-core consumer's prep applies it while transposing (x_slot / y_slot: absmax
   // slots of its big and small operands)
   bool folded = false;
+  // fused skinny chain (tn::ChainDesc): every member carries the chain index (tn_ctx::chains,
+  // -1 = none); the last member launches the whole chain, the others (chained) are skipped
+  int chain = -1;
+  bool chained = false;
+  double chain_tcc = 0, chain_tmc = 0;   // head: the chain's Eq. 4 flops; bytes it moves
   int x_slot = -1, y_slot = -1;
   std::vector<int32_t> pair_map;
   int64_t pair_off = -1;
@@ -154,6 +159,9 @@ struct tn_ctx {
   int64_t g_launch[4] = {0, 0, 0, 0};   // kernel launches per family inside the graph
   int simt_force = -1;          // TN_SIMT_VARIANT=v: every SIMT step uses variant v (tests)
   bool debug_plan = false;      // TN_DEBUG_PLAN=1: print operand layouts while planning
+  int chain_mode = 1;           // TN_CHAIN=0: skinny chains run step by step (A/B, tests)
+  int chain_maxbits = 8;        // TN_CHAIN_MAXBITS: touched bits per carry position
+  double chain_min_save = 0;    // TN_CHAIN_MIN_SAVE_LOG2: HBM bytes a chain must save (2^x elements x 16 B)
   // network
   bool loaded = false, pathed = false, planned = false;
   int n_tensors = 0;
@@ -186,6 +194,11 @@ struct tn_ctx {
   // gate folding decided by a previous planning pass: the folded step's output is not
   // allocated and its inputs stay live until its consumer's prep has read them
   std::vector<char> fold_hint;
+  // fused skinny chains: per step, the chain's launch step if the step is a chained
+  // (not launched) member, else -1; set by one planning pass, honoured by the next (its
+  // output is not materialised, its inputs live until the launch step)
+  std::vector<int> chain_hint;
+  bool replan = false;
   // index reordering (§4.1): 2 = every step's output in its consumer's
   // order (the generalised look-ahead, default), 1 = the paper's top-k rule (Fig. 3),
   // 0 = none (every output in Eq. 3's natural [J][P][Q] order); TN_REORDER / _TOPK
@@ -209,6 +222,9 @@ struct tn_ctx {
   int32_t* d_terms_i = nullptr;
   int64_t* d_terms_s = nullptr;
   tn::EinsumDesc* d_einsum = nullptr;
+  std::vector<tn::ChainDesc> chains;   // host copies (launch parameters)
+  tn::ChainDesc* d_chain = nullptr;
+  int32_t* d_chain_tab = nullptr;
   tn::PrepDesc* d_prep = nullptr;
   float2* d_one = nullptr;
   double* d_partial = nullptr;     // split-K dot partial sums
@@ -288,7 +304,7 @@ void free_dev(tn_ctx* c) {
   void* ptrs[] = {c->d_arena, c->d_scratch, c->d_tables, c->d_acc, c->d_absmax, c->d_scales,
                   c->d_leaf_off, c->d_counter, c->d_out_pos, c->d_slice_desc, c->d_terms_i,
                   c->d_terms_s, c->d_einsum, c->d_prep, c->d_one, c->d_partial, c->d_gt,
-                  c->d_hist, c->d_pexp, c->d_flag, c->d_wave, c->d_gather};
+                  c->d_hist, c->d_pexp, c->d_flag, c->d_wave, c->d_gather, c->d_chain, c->d_chain_tab};
   for (void* p : ptrs) mem_free(c, p);
   c->d_arena = nullptr; c->d_scratch = nullptr; c->d_tables = nullptr; c->d_acc = nullptr;
   c->d_absmax = nullptr; c->d_scales = nullptr; c->d_leaf_off = nullptr; c->d_counter = nullptr;
@@ -298,6 +314,7 @@ void free_dev(tn_ctx* c) {
   c->d_gt = nullptr;
   c->d_hist = nullptr; c->d_pexp = nullptr; c->d_flag = nullptr; c->d_wave = nullptr;
   c->d_gather = nullptr;
+  c->d_chain = nullptr; c->d_chain_tab = nullptr;
   c->planned = false;
 }
 
@@ -842,6 +859,165 @@ void plan_wd_staged(tn::EinsumDesc& e, int64_t nslabs) {
   e.wd_np = np;
   e.wd_nslabs = nslabs;
   e.wd_ok = 1;
+}
+
+// Fused skinny chain (tn::ChainDesc): steps es[0..L-1] are mode-1 skinny
+// einsums, es[i+1] reading es[i]'s output [o][n][v] as its big operand X.  Every index bit
+// gets a global id (the first input's offset bits 0..a-1; an output's v / o bits inherit
+// the ids of the X bits they come from, its n bits are fresh); U = ids some step contracts
+// (k) or creates (n).  Carry bits (first-input ids outside U) pass every step unchanged.
+// Accepted when: every X view is an exact bit permutation of its tensor, offset bits 0-4
+// of the first input and of the last output are the same carry ids (the 32 lanes, unit
+// stride at both ends), <= 32 further carry bits, K <= 16, and every tensor keeps
+// <= maxbits touched bits per carry position.  Fills cd (pointers except tab) and tab.
+bool plan_chain(const std::vector<const tn::EinsumDesc*>& es, int maxbits, tn::ChainDesc& cd,
+                std::vector<int32_t>& tab) {
+  auto lg = [](int64_t x) { int q = 0; while ((int64_t(1) << q) < x) ++q; return q; };
+  auto p2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+  const int L = (int)es.size();
+  if (L < 2 || L > tn::TN_CHAIN_MAX) return false;
+  int next_gid = 0;
+  std::vector<int> prev;                       // gid of each offset bit of the current input
+  std::vector<std::vector<int>> tens;          // gids of T_0 .. T_L by offset bit
+  std::vector<std::vector<int>> kg(L), pog(L), ng(L);
+  std::vector<char> inU(4096, 0);
+  for (int i = 0; i < L; ++i) {
+    const tn::EinsumDesc& e = *es[i];
+    if (e.mode != 1 || e.J != 1 || e.acc || !e.pow2 || e.K > 16 || e.N > 256 || e.N * e.K > 4096) return false;
+    if (!p2(e.N) || !p2(e.K) || !p2(e.V) || !p2(e.M)) return false;
+    // X weights by role: o (innermost digit first), v, k (innermost digit first)
+    std::vector<int64_t> ow, vw, kw;
+    for (int d = e.nm - 2; d >= 0; --d)
+      for (int t = 0; t < e.m_sh[d]; ++t) ow.push_back(e.m_sa[d] << t);
+    for (int t = 0; t < e.m_sh[e.nm - 1]; ++t) vw.push_back(e.m_sa[e.nm - 1] << t);
+    for (int d = e.nk - 1; d >= 0; --d)
+      for (int t = 0; t < e.k_sh[d]; ++t) kw.push_back(e.k_sa[d] << t);
+    const int nb = (int)(ow.size() + vw.size() + kw.size());
+    if ((int64_t(1) << nb) != e.M * e.K) return false;
+    std::vector<int> bitof(nb, -1);            // X offset bit -> role slot
+    auto place = [&](int64_t w) -> int {
+      if (!p2(w)) return -1;
+      const int b = lg(w);
+      if (b >= nb || bitof[b] >= 0) return -1;
+      bitof[b] = 1;
+      return b;
+    };
+    std::vector<int> ob, vb, kb;
+    for (int64_t w : ow) { const int b = place(w); if (b < 0) return false; ob.push_back(b); }
+    for (int64_t w : vw) { const int b = place(w); if (b < 0) return false; vb.push_back(b); }
+    for (int64_t w : kw) { const int b = place(w); if (b < 0) return false; kb.push_back(b); }
+    if (i == 0) {
+      prev.resize(nb);
+      for (int b = 0; b < nb; ++b) prev[b] = next_gid++;
+      tens.push_back(prev);
+    } else if ((int)prev.size() != nb) {
+      return false;                            // X is not exactly the previous output
+    }
+    for (int b : kb) { kg[i].push_back(prev[b]); inU[prev[b]] = 1; }
+    for (int b : vb) pog[i].push_back(prev[b]);
+    for (int b : ob) pog[i].push_back(prev[b]);
+    std::vector<int> out;                      // [o][n][v]: v bits, n bits, o bits
+    for (int b : vb) out.push_back(prev[b]);
+    for (int t = 0; t < lg(e.N); ++t) {
+      const int g = next_gid++;
+      if (g >= 4096) return false;
+      inU[g] = 1;
+      ng[i].push_back(g);
+      out.push_back(g);
+    }
+    for (int b : ob) out.push_back(prev[b]);
+    tens.push_back(out);
+    prev = out;
+  }
+  // working-set index of each tensor: its touched gids in offset-bit order
+  std::vector<std::vector<int>> widx(L + 1);
+  std::vector<std::unordered_map<int, int>> wpos(L + 1);
+  int wmax_a = 0, wmax_b = 0;
+  for (int i = 0; i <= L; ++i) {
+    for (int g : tens[i]) if (inU[g]) { wpos[i][g] = (int)widx[i].size(); widx[i].push_back(g); }
+    if ((int)widx[i].size() > maxbits) return false;
+    if (i % 2 == 0) wmax_a = std::max(wmax_a, (int)widx[i].size());
+    else wmax_b = std::max(wmax_b, (int)widx[i].size());
+  }
+  // lanes: the 5 lowest-weight carry bits of T0 (ideally T0's and TL's offset bits 0-4:
+  // unit-stride lanes at both ends; otherwise the lanes stride and L1 merges the sectors)
+  const std::vector<int>& T0 = tens[0];
+  const std::vector<int>& TL = tens[L];
+  std::unordered_map<int, int> tl_bit;
+  for (int b = 0; b < (int)TL.size(); ++b) tl_bit[TL[b]] = b;
+  int nct = 0, nl = 0;
+  for (int b = 0; b < (int)T0.size(); ++b) {
+    if (inU[T0[b]]) continue;
+    auto it = tl_bit.find(T0[b]);
+    if (it == tl_bit.end()) return false;
+    if (nl < 5) {
+      cd.lw_src[nl] = int64_t(1) << b;
+      cd.lw_dst[nl] = int64_t(1) << it->second;
+      ++nl;
+      continue;
+    }
+    if (nct >= 32) return false;
+    cd.ct_src[nct] = int64_t(1) << b;
+    cd.ct_dst[nct] = int64_t(1) << it->second;
+    ++nct;
+  }
+  if (nl < 5) return false;
+  // both ends must stay reasonably local: a 32-lane access spans <= 8 KiB (the tile's other
+  // touched elements fill the rest of those sectors from L1)
+  if (cd.lw_src[4] > 512 || cd.lw_dst[4] > 512) return false;
+  cd.nct = nct;
+  cd.n_tiles = int64_t(1) << nct;
+  cd.L = L;
+  cd.a0 = (int)widx[0].size();
+  cd.aL = (int)widx[L].size();
+  cd.buf_a = 1 << wmax_a;
+  cd.buf_b = 1 << wmax_b;
+  tab.clear();
+  std::unordered_map<int, int> t0_bit;
+  for (int b = 0; b < (int)T0.size(); ++b) t0_bit[T0[b]] = b;
+  for (int x = 0; x < (1 << cd.a0); ++x) {     // t0off
+    int64_t o = 0;
+    for (int j = 0; j < cd.a0; ++j) if ((x >> j) & 1) o += int64_t(1) << t0_bit[widx[0][j]];
+    if (o > INT32_MAX) return false;
+    tab.push_back((int32_t)o);
+  }
+  for (int x = 0; x < (1 << cd.aL); ++x) {     // tLoff
+    int64_t o = 0;
+    for (int j = 0; j < cd.aL; ++j) if ((x >> j) & 1) o += int64_t(1) << tl_bit[widx[L][j]];
+    if (o > INT32_MAX) return false;
+    tab.push_back((int32_t)o);
+  }
+  for (int i = 0; i < L; ++i) {
+    const tn::EinsumDesc& e = *es[i];
+    tn::ChainStep& st = cd.st[i];
+    std::vector<int> pt;                       // touched o / v ids: the o-positions
+    for (int g : pog[i]) if (inU[g]) pt.push_back(g);
+    st.N = (int32_t)e.N;
+    st.K = (int32_t)e.K;
+    st.P = 1 << (int)pt.size();
+    st.in_buf = i % 2;
+    st.tab = (int32_t)tab.size();
+    auto wsum = [&](int x, const std::vector<int>& gids, const std::unordered_map<int, int>& pos) {
+      int32_t o = 0;
+      for (size_t j = 0; j < gids.size(); ++j) if ((x >> j) & 1) o += 1 << pos.at(gids[j]);
+      return o;
+    };
+    for (int x = 0; x < st.P; ++x) tab.push_back(wsum(x, pt, wpos[i]));          // in_p
+    for (int x = 0; x < st.P; ++x) tab.push_back(wsum(x, pt, wpos[i + 1]));      // out_p
+    for (int x = 0; x < st.K; ++x) tab.push_back(wsum(x, kg[i], wpos[i]));       // in_k
+    for (int x = 0; x < st.N; ++x) tab.push_back(wsum(x, ng[i], wpos[i + 1]));   // out_n
+    for (int n = 0; n < st.N; ++n)                                               // yoff[n][k]
+      for (int k = 0; k < st.K; ++k) {
+        int64_t o = 0, t = n;
+        for (int d = e.nn - 1; d >= 0; --d) { o += (t & ((int64_t(1) << e.n_sh[d]) - 1)) * e.n_sb[d]; t >>= e.n_sh[d]; }
+        t = k;
+        for (int d = e.nk - 1; d >= 0; --d) { o += (t & ((int64_t(1) << e.k_sh[d]) - 1)) * e.k_sb[d]; t >>= e.k_sh[d]; }
+        if (o > INT32_MAX) return false;
+        tab.push_back((int32_t)o);
+      }
+  }
+  cd.n_tab = (int32_t)tab.size();
+  return tn::chain_smem_bytes(cd) <= 110 * 1024;
 }
 
 void contiguous_strides(std::vector<VDim>& d) {
@@ -1406,10 +1582,13 @@ tn_status build_plan(tn_ctx* c) {
       sp.g_blk_off = (int64_t)tables.size();
       tables.insert(tables.end(), sp.g_blk.begin(), sp.g_blk.end());
     }
-    const bool hinted = s < (int)c->fold_hint.size() && c->fold_hint[s] && consumer_step[s] > s;
+    const bool fold_hinted = s < (int)c->fold_hint.size() && c->fold_hint[s] && consumer_step[s] > s;
+    const int chain_at = s < (int)c->chain_hint.size() ? c->chain_hint[s] : -1;
+    const bool hinted = fold_hinted || chain_at > s;
+    const int keep_to = fold_hinted ? consumer_step[s] : chain_at;   // inputs released there
     if (!sp.final_step) {
       sp.out_elems = out_elems;
-      sp.out_off = hinted ? 0 : arena.alloc(out_elems);   // folded: never materialised
+      sp.out_off = hinted ? 0 : arena.alloc(out_elems);   // folded / chained: never materialised
       out.off = sp.out_off;
     }
     if (sp.tc) {
@@ -1435,8 +1614,8 @@ tn_status build_plan(tn_ctx* c) {
     // release consumed arena inputs (their only consumer is this step); a folded step's
     // inputs are read by its consumer's prep, so they are released there
     if (hinted) {
-      if (A.buf == 1) deferred[consumer_step[s]].push_back(A.off);
-      if (B.buf == 1) deferred[consumer_step[s]].push_back(B.off);
+      if (A.buf == 1 && !(s > 0 && folded_out(sp.i))) deferred[keep_to].push_back(A.off);
+      if (B.buf == 1 && !(s > 0 && folded_out(sp.j))) deferred[keep_to].push_back(B.off);
     } else {
       if (A.buf == 1 && !(s > 0 && folded_out(sp.i))) arena.release(A.off);
       if (B.buf == 1 && !(s > 0 && folded_out(sp.j))) arena.release(B.off);
@@ -1561,9 +1740,17 @@ tn_status build_plan(tn_ctx* c) {
   char errbuf[256];
   std::unordered_map<int, int> producer_of;     // live tensor id -> producing step
   std::vector<std::array<int, 2>> side_producer(n_steps, {-1, -1});   // per TC side
+  std::vector<int> x_producer(n_steps, -1);     // skinny steps: producer of the big operand X
+  std::vector<int> y_producer(n_steps, -1);     // ... and of the small operand Y
   for (int s = 0; s < n_steps; ++s) {
     StepPlan& sp = c->steps[s];
     View A = live[sp.i], B = live[sp.j];
+    if (!sp.tc && sp.mode == 1) {
+      auto it = producer_of.find(sp.x_is_b ? sp.j : sp.i);
+      x_producer[s] = it == producer_of.end() ? -1 : it->second;
+      auto iy = producer_of.find(sp.x_is_b ? sp.i : sp.j);
+      y_producer[s] = iy == producer_of.end() ? -1 : iy->second;
+    }
     if (sp.tc)
       for (int side = 0; side < 2; ++side) {
         const int id = ((side == 0) != sp.swap) ? sp.i : sp.j;
@@ -2085,9 +2272,158 @@ tn_status build_plan(tn_ctx* c) {
       return TN_OK;
     }
   }
+  // ---- fused skinny chains: maximal runs of skinny steps feeding each
+  // other's big operand, cut greedily where plan_chain rejects the extension
+  c->chains.clear();
+  std::vector<int32_t> chain_tab_all;
+  std::vector<int32_t> chain_tab_at;
+  for (auto& sp : c->steps) { sp.chain = -1; sp.chained = false; }
+  if (c->chain_mode) {
+    auto ok = [&](int s) {
+      const StepPlan& sp = c->steps[s];
+      return !sp.tc && !sp.folded && sp.mode == 1 && !sp.final_step && sp.J == 1 && sp.einsum_idx >= 0;
+    };
+    auto unmaterialised = [&](int w) {
+      return c->steps[w].folded || (w < (int)c->chain_hint.size() && c->chain_hint[w] > w);
+    };
+    auto overlaps = [&](int w, int p) {     // step w's output slot overlaps step p's output slot
+      const StepPlan& W = c->steps[w];
+      const StepPlan& P = c->steps[p];
+      if (W.final_step || unmaterialised(w) || P.final_step) return false;
+      return W.out_off < P.out_off + P.out_elems && P.out_off < W.out_off + W.out_elems;
+    };
+    auto chain_inputs_survive = [&](const std::vector<int>& run, size_t a, size_t b) {
+      const int last = run[b - 1];
+      std::vector<char> member(n_steps, 0);
+      for (size_t q = a; q < b; ++q) member[run[q]] = 1;
+      std::vector<std::pair<int, int>> ins;  // (producer of the input, step consuming it)
+      ins.push_back({x_producer[run[a]], run[a]});
+      for (size_t q = a; q < b; ++q) ins.push_back({y_producer[run[q]], run[q]});
+      for (auto& in : ins) {
+        if (in.first < 0) continue;          // a leaf: never overwritten
+        for (int w = in.second + 1; w < last; ++w)
+          if (!member[w] && overlaps(w, in.first)) return false;
+      }
+      return true;
+    };
+    std::vector<int> nxt(n_steps, -1), has_prev(n_steps, 0);
+    for (int s = 0; s < n_steps; ++s) {
+      const int cn = consumer_step[s];
+      if (ok(s) && cn >= 0 && ok(cn) && x_producer[cn] == s) { nxt[s] = cn; has_prev[cn] = 1; }
+    }
+    for (int s0 = 0; s0 < n_steps; ++s0) {
+      if (nxt[s0] < 0 || has_prev[s0]) continue;
+      std::vector<int> run;
+      for (int s = s0; s >= 0; s = nxt[s]) run.push_back(s);
+      // partition the run into chains maximising the HBM bytes saved (each intermediate of a
+      // chain is neither written nor read back): DP over accepted sub-chains [a, b)
+      const size_t R = run.size();
+      std::vector<double> gain(R + 1, 0.0);
+      std::vector<size_t> cut(R + 1, 0);
+      for (size_t a = R; a-- > 0;) {
+        gain[a] = gain[a + 1];
+        cut[a] = a + 1;          // a alone
+        double saved = 0.0;
+        for (size_t b = a + 2; b <= R && b - a <= (size_t)tn::TN_CHAIN_MAX; ++b) {
+          const tn::EinsumDesc& em = eds[c->steps[run[b - 2]].einsum_idx];
+          saved += 16.0 * (double)(em.M * em.N);   // intermediate run[b-2] -> run[b-1]
+          std::vector<const tn::EinsumDesc*> es;
+          for (size_t q = a; q < b; ++q) es.push_back(&eds[c->steps[run[q]].einsum_idx]);
+          tn::ChainDesc cd;
+          memset(&cd, 0, sizeof(cd));
+          std::vector<int32_t> tab;
+          // profitable only when the chain keeps a big intermediate out of HBM: measured on
+          // C4-sparse, a chain saving 2^30+2^29 elements wins (11.1 -> 9.5 ms), one saving
+          // 2^28+2^29 breaks even and small ones lose (the per-tile barriers and load latency
+          // of the fused kernel outweigh the traffic)
+          // ... and each tile must carry enough work (>= 64 touched elements in some tensor)
+          if (saved >= c->chain_min_save && plan_chain(es, c->chain_maxbits, cd, tab) &&
+              std::max(cd.buf_a, cd.buf_b) >= 64 && saved + gain[b] > gain[a]) {
+            gain[a] = saved + gain[b];
+            cut[a] = b;
+          }
+        }
+      }
+      for (size_t a = 0; a < R;) {
+        const size_t best = cut[a];
+        if (best == a + 1) { a = best; continue; }
+        // the chain runs at its last member's position: its inputs (the head's X, every
+        // member's Y) must have survived until then (the hinted pass keeps them live)
+        if (!c->chain_hint.empty() && !chain_inputs_survive(run, a, best))
+          return fail(TN_ERR_INTERNAL, "chain inputs not kept live");
+        tn::ChainDesc bd;
+        memset(&bd, 0, sizeof(bd));
+        std::vector<int32_t> btab;
+        {
+          std::vector<const tn::EinsumDesc*> es;
+          for (size_t q = a; q < best; ++q) es.push_back(&eds[c->steps[run[q]].einsum_idx]);
+          if (!plan_chain(es, c->chain_maxbits, bd, btab)) return fail(TN_ERR_INTERNAL, "chain re-plan");
+        }
+        const tn::EinsumDesc& e0 = eds[c->steps[run[a]].einsum_idx];
+        const tn::EinsumDesc& eL = eds[c->steps[run[best - 1]].einsum_idx];
+        bd.src = e0.A; bd.src_off = e0.a_off; bd.src_leaf = e0.a_leaf;
+        bd.dst = eL.C; bd.absmax_out = eL.absmax_out;
+        for (size_t q = a; q < best; ++q) {
+          const tn::EinsumDesc& e = eds[c->steps[run[q]].einsum_idx];
+          bd.st[q - a].Y = e.B; bd.st[q - a].y_off = e.b_off; bd.st[q - a].y_leaf = e.b_leaf;
+          c->steps[run[q]].chained = q + 1 < best;    // launched at the last member's position
+          c->steps[run[q]].chain = (int)c->chains.size();
+        }
+        const int at = run[best - 1];
+        c->steps[at].chain = (int)c->chains.size();
+        {
+          double t = 0, y = 0;
+          for (size_t q = a; q < best; ++q) {
+            t += c->steps[run[q]].tcc;
+            y += 8.0 * eds[c->steps[run[q]].einsum_idx].N * eds[c->steps[run[q]].einsum_idx].K;
+          }
+          c->steps[at].chain_tcc = t;
+          c->steps[at].chain_tmc = 8.0 * (double)(e0.M * e0.K + eL.M * eL.N) + y;
+        }
+        chain_tab_at.push_back((int32_t)chain_tab_all.size());
+        chain_tab_all.insert(chain_tab_all.end(), btab.begin(), btab.end());
+        c->chains.push_back(bd);
+        if (c->debug_plan) {
+          fprintf(stderr, "[tn] chain:");
+          for (size_t q = a; q < best; ++q) fprintf(stderr, " %d", run[q]);
+          fprintf(stderr, " (W bits %d..%d, carry tiles 2^%d, smem %zu B)\n", bd.a0, bd.aL, bd.nct,
+                  tn::chain_smem_bytes(bd));
+        }
+        a = best;
+      }
+    }
+  }
+  {
+    std::vector<int> hint(n_steps, -1);
+    for (int q = 0; q < n_steps; ++q)
+      if (c->steps[q].chained) {
+        int L = q;
+        while (L < n_steps && !(c->steps[L].chain == c->steps[q].chain && !c->steps[L].chained)) ++L;
+        hint[q] = L;
+      }
+    const bool any = std::any_of(hint.begin(), hint.end(), [](int x) { return x >= 0; });
+    if (c->chain_hint.empty()) {
+      if (any) {                       // re-plan with the chains' liveness (tn_set_slices)
+        c->chain_hint = hint;
+        c->replan = true;
+        return TN_OK;
+      }
+    } else if (hint != c->chain_hint) {
+      return fail(TN_ERR_INTERNAL, "skinny chains changed between planning passes");
+    }
+  }
   if (c->host_only) {
     c->planned = true;
     return TN_OK;
+  }
+  if (!c->chains.empty()) {
+    if (tn_status st3 = dev_alloc(c, &c->d_chain, c->chains.size())) return st3;
+    if (tn_status st3 = dev_alloc(c, &c->d_chain_tab, chain_tab_all.size())) return st3;
+    TN_CUDA(cudaMemcpyAsync(c->d_chain_tab, chain_tab_all.data(), chain_tab_all.size() * 4,
+                            cudaMemcpyHostToDevice, sm));
+    for (size_t q = 0; q < c->chains.size(); ++q) c->chains[q].tab = c->d_chain_tab + chain_tab_at[q];
+    TN_CUDA(cudaMemcpyAsync(c->d_chain, c->chains.data(), c->chains.size() * sizeof(tn::ChainDesc),
+                            cudaMemcpyHostToDevice, sm));
   }
   if (n_einsum) TN_CUDA(cudaMemcpyAsync(c->d_einsum, eds.data(), n_einsum * sizeof(tn::EinsumDesc),
                                         cudaMemcpyHostToDevice, sm));
@@ -2144,6 +2480,12 @@ tn_status launch_slice(tn_ctx* c, const std::vector<int>& passes, cudaStream_t s
   for (size_t s = 0; s < c->steps.size(); ++s) {
     StepPlan& sp = c->steps[s];
     if (!sp.tc && sp.folded) continue;      // applied inside its consumer's prep
+    if (!sp.tc && sp.chained) continue;     // computed inside its chain's launch
+    if (!sp.tc && sp.chain >= 0) {          // fused skinny chain ending at this step
+      Timer tm(c, 2, sp.chain_tcc, sp.chain_tmc, (int)s, sm);
+      TN_CUDA(tn::launch_chain(c->d_chain + sp.chain, c->chains[sp.chain], c->d_leaf_off, sm));
+      continue;
+    }
     if (!sp.tc) {
       // first execution of an HBM-bound SIMT step: time every kernel variant on the
       // live operands (the step is idempotent unless it accumulates) and keep the
@@ -2375,6 +2717,9 @@ tn_status tn_create(tn_ctx** out, int device, const tn_allocator* allocator, voi
     tn_ctx* c = new tn_ctx();
     c->host_only = true;
     c->debug_plan = env_int("TN_DEBUG_PLAN", 0) != 0;
+    c->chain_mode = env_int("TN_CHAIN", 1);
+    c->chain_maxbits = env_int("TN_CHAIN_MAXBITS", 8);
+    c->chain_min_save = 16.0 * std::ldexp(1.0, env_int("TN_CHAIN_MIN_SAVE_LOG2", 30));
     c->device = -1;
     *out = c;
     return TN_OK;
@@ -2401,6 +2746,10 @@ tn_status tn_create(tn_ctx** out, int device, const tn_allocator* allocator, voi
   c->use_graphs = env_int("TN_GRAPHS", 1) != 0;
   c->simt_force = env_int("TN_SIMT_VARIANT", -1);
   c->group_m = env_int("TN_GEMM_GROUP", 8);   // best of {1,8,16,32} on 8192^2 x 16384
+  c->debug_plan = env_int("TN_DEBUG_PLAN", 0) != 0;
+  c->chain_mode = env_int("TN_CHAIN", 1);
+  c->chain_maxbits = env_int("TN_CHAIN_MAXBITS", 8);
+  c->chain_min_save = 16.0 * std::ldexp(1.0, env_int("TN_CHAIN_MIN_SAVE_LOG2", 30));
   *out = c;
   return TN_OK;
 }
@@ -2570,9 +2919,19 @@ tn_status tn_set_slices(tn_ctx* c, int32_t n_sliced, const int64_t* sliced_label
   // planning runs twice when gate folding applies: the first pass decides the folds,
   // the second keeps the folded steps' inputs live until their consumers (fold_hint)
   c->fold_hint.clear();
+  c->chain_hint.clear();
+  c->replan = false;
   tn_status st = build_plan(c);
   if (!st && !c->fold_hint.empty()) st = build_plan(c);
-  if (st) { free_dev(c); c->fold_hint.clear(); return st; }
+  // skinny chains are decided once the folds are: one more pass keeps their inputs live
+  if (!st && c->replan) { c->replan = false; st = build_plan(c); }
+  if (!st && c->replan) { c->replan = false; st = build_plan(c); }
+  if (st || c->replan) {
+    free_dev(c);
+    c->fold_hint.clear();
+    c->chain_hint.clear();
+    return st ? st : fail(TN_ERR_INTERNAL, "planning did not converge");
+  }
   if (n_slices_out) *n_slices_out = c->n_slices;
   return TN_OK;
 }
@@ -2675,14 +3034,14 @@ tn_status tn_plan_json(tn_ctx* c, char* buf, size_t cap, size_t* len) {
     snprintf(b, sizeof(b),
              "{\"i\":%d,\"j\":%d,\"J\":%lld,\"m\":%lld,\"n\":%lld,\"k\":%lld,\"tcc\":%.17g,"
              "\"tmc\":%.17g,\"route\":\"%s\",\"swap\":%s,\"mode\":%d,\"grouped\":%s,"
-             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"folded\":%s,\"wd_staged\":%s,\"ia\":",
+             "\"gathered_rows\":%lld,\"out_gen\":%s,\"prep\":[%d,%d],\"planes_out\":%s,\"dense_merge\":%s,\"folded\":%s,\"wd_staged\":%s,\"chain\":%d,\"chained\":%s,\"ia\":",
              sp.i, sp.j, (long long)sp.J, (long long)sp.m, (long long)sp.n, (long long)sp.k, sp.tcc,
              sp.tmc, sp.tc ? "tcgen05" : "simt", sp.swap ? "true" : "false", sp.mode,
              sp.grouped ? "true" : "false", (long long)sp.g_rows, sp.out_gen ? "true" : "false",
              sp.tc ? (sp.skip_prep[0] ? -1 : sp.r_fast[0]) : -1,
              sp.tc ? (sp.skip_prep[1] ? -1 : sp.r_fast[1]) : -1, sp.planes_consumer >= 0 ? "true" : "false",
              sp.dense_merge ? "true" : "false", sp.folded ? "true" : "false",
-             (!sp.tc && sp.hdesc.wd_ok) ? "true" : "false");
+             (!sp.tc && sp.hdesc.wd_ok) ? "true" : "false", sp.chain, sp.chained ? "true" : "false");
     o += b;
     if (sp.merge) json_u64_list(o, sp.ia); else o += "null";
     o += ",\"ib\":";

@@ -50,6 +50,33 @@ struct EinsumDesc {
   int32_t wd_ptop[8];             // part index -> canonical output column offset
 };
 
+// ---------------------------------------------------------------- fused skinny chain
+// A chain of skinny SIMT steps s1 -> s2 -> ... -> sL on the stem (each consumes the
+// previous output as its big operand X and absorbs a small tensor Y) run as ONE pass:
+// the index bits no step touches ("carry" bits) enumerate independent positions; for a
+// tile of 32 carry positions (lanes = the 5 lowest-weight carry bits of the first input
+// T0) a block loads T0's touched elements, runs every
+// step in shared memory ([touched index][32 lanes] tensors) and writes TL.  Each output
+// is the same fp32 k-ordered sum as einsum_skinny_kernel, so the result is bit-identical
+// to running the steps one by one; the intermediates never reach HBM.
+constexpr int TN_CHAIN_MAX = 8;
+struct ChainStep {
+  const float2* Y; int64_t y_off; int32_t y_leaf;
+  int32_t N, K, P;                // outputs per o-position, k, touched o-positions
+  int32_t tab;                    // int32 table offset: in_p[P], out_p[P], in_k[K], out_n[N], yoff[N*K]
+  int32_t in_buf, pad_;           // smem buffer holding the step's input (0 = A, 1 = B)
+};
+struct ChainDesc {
+  const float2* src; int64_t src_off; int32_t src_leaf, L;
+  float2* dst; unsigned* absmax_out;
+  int32_t a0, aL, nct, buf_a, buf_b, n_tab;   // log2 |W0|, log2 |WL|, outer carry bits, buffer elems
+  int64_t n_tiles;
+  int64_t ct_src[32], ct_dst[32];             // outer carry bit weights in T0 / TL
+  int64_t lw_src[5], lw_dst[5];               // the 5 lane carry bits' weights in T0 / TL
+  const int32_t* tab;                         // t0off[2^a0], tLoff[2^aL], then the step tables
+  ChainStep st[TN_CHAIN_MAX];
+};
+
 // ---------------------------------------------------------------- operand prep
 // Permute a strided complex64 view into K-contiguous fp16 planes with a
 // per-tensor power-of-two scale: plane p of element (g, r, k) at
@@ -202,6 +229,9 @@ cudaError_t launch_prep(const PrepDesc* d_desc, int64_t total, int planes, int k
 cudaError_t launch_einsum(const EinsumDesc* d_desc, const EinsumDesc& host_desc,
                           const int64_t* leaf_off, cudaStream_t s, int variant = 0);
 int einsum_variants(const EinsumDesc& host_desc);
+cudaError_t launch_chain(const ChainDesc* d_desc, const ChainDesc& host_desc, const int64_t* leaf_off,
+                         cudaStream_t s);
+size_t chain_smem_bytes(const ChainDesc& host_desc);
 cudaError_t launch_gather_out(const double2* acc, const int32_t* pos, double2* out, int64_t n,
                               const int* flag, cudaStream_t s);
 cudaError_t launch_absmax(const float2* x, int64_t n, unsigned* out, cudaStream_t s);

@@ -210,3 +210,53 @@ def test_reorder_modes_change_layout_not_bookkeeping(monkeypatch):
         c, pj = _check_plan(w)
         gens[mode] = sum(1 for s in pj["steps"] if s["out_gen"])
     assert gens[0] == 0 and gens[0] <= gens[1] <= gens[2] and gens[2] > 0
+
+
+def test_skinny_chains_c4_sparse(monkeypatch):
+    """Fused skinny chains on the headline plan: stem chains are found
+    (263 -> 264 -> 266 and 280 -> 282 -> 283 among them); every member is a skinny (mode 1)
+    SIMT step whose big operand is the previous member's output; only the last member of a
+    chain is launched (the others are marked chained)."""
+    w = configs.c4("sparse16", 32)
+    monkeypatch.setenv("TN_CHAIN_MIN_SAVE_LOG2", "0")    # every eligible chain
+    c = Contraction(device=-1)
+    c.setup(w.net, w.samples, w.path, w.sliced)
+    steps = c.plan_json()["steps"]
+    runs = {}
+    for i, s in enumerate(steps):
+        if s["chain"] >= 0:
+            runs.setdefault(s["chain"], []).append(i)
+    assert [263, 264, 266] in runs.values(), runs
+    assert [280, 282, 283] in runs.values(), runs
+    for run in runs.values():
+        assert len(run) >= 2
+        assert [steps[t]["chained"] for t in run] == [True] * (len(run) - 1) + [False]
+        for a, b in zip(run, run[1:]):
+            assert a in (_producer(steps, b, steps[b]["i"]), _producer(steps, b, steps[b]["j"]))
+        for t in run:
+            assert steps[t]["route"] == "simt" and steps[t]["mode"] == 1 and not steps[t]["folded"]
+
+
+def _producer(steps, s, tid):
+    """Step that produced live tensor id `tid` before step s (stable ids: result keeps i)."""
+    for q in range(s - 1, -1, -1):
+        if steps[q]["i"] == tid:
+            return q
+    return -1
+
+
+def test_skinny_chains_off_keeps_bookkeeping(monkeypatch):
+    w = configs.c4("sparse16", 32)
+    monkeypatch.setenv("TN_CHAIN", "0")
+    c0 = Contraction(device=-1)
+    c0.setup(w.net, w.samples, w.path, w.sliced)
+    s0 = c0.plan_json()["steps"]
+    monkeypatch.setenv("TN_CHAIN", "1")
+    c1 = Contraction(device=-1)
+    c1.setup(w.net, w.samples, w.path, w.sliced)
+    s1 = c1.plan_json()["steps"]
+    assert not any(s["chain"] >= 0 or s["chained"] for s in s0)
+    assert any(s["chained"] for s in s1)
+    for a, b in zip(s0, s1):
+        for key in ["i", "j", "J", "m", "n", "k", "tcc", "tmc", "route", "mode"]:
+            assert a[key] == b[key]

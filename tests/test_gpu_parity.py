@@ -509,3 +509,45 @@ def test_lxeb_of_gpu_amplitudes(ctx):
     assert abs(f_gpu - f_ref) <= 1e-5 * abs(f_ref + 1.0)
     assert abs(f_gpu - 1.0) < 5 * verify.lxeb_stderr(amps[exact], n)
     assert abs(verify.lxeb(amps[uniform], n)) < 5 * verify.lxeb_stderr(amps[uniform], n)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("boundary", ["sparse16", "single"])
+def test_skinny_chains_match_unchained(ctx, boundary, monkeypatch):
+    """Fused skinny chains at full width: one sub-network slice of the C4
+    order run with the chains (TN_CHAIN=1, default) and step by step (TN_CHAIN=0).  Each
+    chained output is the same fp32 k-ordered sum as the skinny kernel's, so the two agree
+    to rounding-order noise; both are checked against the oracle."""
+    from tnworkloads.network import Network, fix_bonds
+    w = configs.c4(boundary, 32)
+    fine, pc = _refine(w, 2e11 if boundary == "sparse16" else 3e11)
+    extra = fine[len(w.sliced):]
+    sub = fix_bonds(w.net, {x: 0 for x in extra})
+    ref0 = oracle.contract_slice(sub, w.path, w.sliced, 0, w.samples)
+    # multilinear rescaling (DESIGN.md §7e): this sub-network's result is tiny enough that
+    # complex64 intermediates lose precision on either route
+    c_ = float(np.abs(ref0).max()) ** (-1.0 / sub.n_tensors)
+    sub = Network([tt * c_ for tt in sub.tensors], sub.labels, sub.dims, sub.open_labels, sub.n_qubits,
+                  sub.coords)
+    ref = ref0 * c_ ** sub.n_tensors
+    monkeypatch.setenv("TN_AUTOTUNE", "0")        # the same skinny kernel variant in both runs
+    monkeypatch.setenv("TN_CHAIN_MIN_SAVE_LOG2", "0")   # every eligible chain, not only profitable ones
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TN_CHAIN", mode)
+        c = Contraction(device=0, stream=torch.cuda.current_stream())
+        c.setup(sub, w.samples, w.path, w.sliced)
+        steps = c.plan_json()["steps"]
+        c.contract(0, 1)
+        outs[mode] = c.sum_slices_host()
+        c.close()
+        if mode == "1":
+            n_chained = sum(s["chained"] for s in steps)
+    d = rel_l2(outs["1"], outs["0"])
+    e0, e1 = rel_l2(outs["0"], ref), rel_l2(outs["1"], ref)
+    print(f"C4 {boundary} chains: {n_chained} chained steps, chained vs unchained {d:.2e}, "
+          f"vs oracle {e1:.3e} / {e0:.3e}")
+    assert n_chained > 2
+    assert d <= 1e-6
+    assert e1 <= e0 * 1.01 + 1e-12
+    assert e1 <= EXT_TOL

@@ -1,0 +1,6 @@
+# short-K promotion interval: A = default (every k-block), B = TN_KCHUNK3_SHORT=2 for K <= 512;
+# time (A/B step profiles) and error (full-width sub-slice parity tests under B)
+AB_ENV_B="TN_KCHUNK3_SHORT=2" bash tools/gpu_ab.sh
+TN_KCHUNK3_SHORT=2 timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout=900 -p no:cacheprovider -s \
+    -k "c4_bench or sparse_state or c5_m20" > gpurun_out/pytest_kchunk2.log 2>&1; echo pytest_rc=$?
+grep -E "sub-slice|sub-network|passed|failed" gpurun_out/pytest_kchunk2.log | tail -8

@@ -12,4 +12,8 @@ for job in $NCU_JOBS; do
   timeout 900 ncu --profile-from-start off -k regex:$kre --launch-skip $skip --launch-count 1 --set full \
       --import-source on --clock-control none -o gpurun_out/ncu_$name -f \
       python tools/ncu_step.py --boundary ${BOUNDARY:-sparse16} --step $step > gpurun_out/ncu_$name.log 2>&1; echo ncu_rc=$?
+  # summaries travel back (gpurun_out is capped at 64 MiB): raw metrics + per-line stalls
+  ncu -i gpurun_out/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu_${name}_raw.csv 2>/dev/null
+  python tools/ncu_lines.py gpurun_out/ncu_$name.ncu-rep 40 > gpurun_out/ncu_${name}_lines.txt 2>&1
+  [ -z "$KEEP_REP" ] && rm -f gpurun_out/ncu_$name.ncu-rep
 done
