@@ -1724,7 +1724,8 @@ __global__ void __launch_bounds__(CH_THREADS) einsum_chain_kernel(const ChainDes
   float2* Ys = bufB + 32 * (size_t)d.buf_b;
   int ysz = 0;
   for (int i = 0; i < d.L; ++i) ysz += (d.st[i].N * d.st[i].K + 1) & ~1;
-  int32_t* tab = reinterpret_cast<int32_t*>(Ys + ysz);
+  const size_t ysz_al = (size_t)ysz;
+  int32_t* tab = reinterpret_cast<int32_t*>(Ys + ysz + 2 * 32 * ((size_t)1 << d.a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < d.n_tab; i += CH_THREADS) tab[i] = d.tab[i];
   __syncthreads();
@@ -1748,19 +1749,29 @@ __global__ void __launch_bounds__(CH_THREADS) einsum_chain_kernel(const ChainDes
   const int32_t* t0off = tab;
   const int32_t* tLoff = tab + n0;
   float amax = 0.f;
+  // the input tile is double-buffered: tile t + grid is loaded (8-B LDGSTS, all in flight)
+  // while tile t runs its steps; step 0 reads W0 straight from the load buffer
+  float2* w0buf[2] = {Ys + ysz_al, Ys + ysz_al + 32 * (size_t)n0};
+  auto issue = [&](int64_t t, float2* dst) {
+    int64_t cs_, cd_;
+    tile_bits_sum(tb, (uint64_t)t, lane, d.nct, d.ct_src, d.ct_dst, cs_, cd_);
+    const float2* sp = src + cs_ + ls;
+    for (int e = warp; e < n0; e += CH_THREADS / 32) cp_async8(dst + e * 32 + lane, sp + t0off[e]);
+  };
+  __syncthreads();                   // Y staged
+  if (blockIdx.x < d.n_tiles) issue(blockIdx.x, w0buf[0]);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int cur = 0;
   for (int64_t t = blockIdx.x; t < d.n_tiles; t += gridDim.x) {
     int64_t cs, cdst;
     tile_bits_sum(tb, (uint64_t)t, lane, d.nct, d.ct_src, d.ct_dst, cs, cdst);
-    __syncthreads();                 // Y staged / previous tile's W_L stored
-    const float2* sp = src + cs + ls;
-    // every load of the tile in flight at once (8-B LDGSTS straight into W0)
-    for (int e = warp; e < n0; e += CH_THREADS / 32) cp_async8(bufA + e * 32 + lane, sp + t0off[e]);
-    cp_async_wait_all();
-    __syncthreads();
+    if (t + gridDim.x < d.n_tiles) issue(t + gridDim.x, w0buf[cur ^ 1]);
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
+    __syncthreads();                 // tile t's input complete for every thread
     int yo = 0;
     for (int i = 0; i < d.L; ++i) {
       const ChainStep& st = d.st[i];
-      const float2* W = st.in_buf ? bufB : bufA;
+      const float2* W = i == 0 ? w0buf[cur] : (st.in_buf ? bufB : bufA);
       float2* O = st.in_buf ? bufA : bufB;
       const int32_t* in_p = tab + st.tab;
       const int32_t* out_p = in_p + st.P;
@@ -1785,7 +1796,10 @@ __global__ void __launch_bounds__(CH_THREADS) einsum_chain_kernel(const ChainDes
       dp[tLoff[e]] = v;
       amax = fmaxf(amax, fmaxf(fabsf(v.x), fabsf(v.y)));
     }
+    cur ^= 1;
+    __syncthreads();                 // W_L read before the next tile's steps overwrite it
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (d.absmax_out) block_absmax(amax, d.absmax_out);
 }
 
@@ -2124,7 +2138,8 @@ void launch_wide(const EinsumDesc* d_desc, const EinsumDesc& h, const int64_t* l
 size_t chain_smem_bytes(const ChainDesc& d) {
   size_t ys = 0;
   for (int i = 0; i < d.L; ++i) ys += ((size_t)d.st[i].N * d.st[i].K + 1) & ~(size_t)1;
-  return sizeof(float2) * (32 * ((size_t)d.buf_a + d.buf_b) + ys) + sizeof(int32_t) * (size_t)d.n_tab;
+  return sizeof(float2) * (32 * ((size_t)d.buf_a + d.buf_b + 2 * ((size_t)1 << d.a0)) + ys) +
+         sizeof(int32_t) * (size_t)d.n_tab;
 }
 
 cudaError_t launch_chain(const ChainDesc* d_desc, const ChainDesc& h, const int64_t* leaf_off, cudaStream_t s) {

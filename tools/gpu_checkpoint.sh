@@ -6,7 +6,8 @@ timeout 1800 python -m pytest tests -m gpu -q --timeout=900 -p no:cacheprovider 
 tail -1 gpurun_out/pytest_gpu.log; grep -E "^FAILED|^E  " gpurun_out/pytest_gpu.log | head -10
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
-for extra in "--boundary single" "--precision mixed" "--workload c5 --boundary single --steps 5"; do
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.json 2>/dev/null; echo "bench reference rc=$?"
+for extra in "--boundary single" "--precision mixed" "--workload c5 --boundary single --steps 5" "--order-tag a64b1 --steps 5"; do
   tag=$(echo $extra | tr -d ' -' | cut -c1-24)
   timeout 900 python bench.py $extra --no-cpu-baseline > gpurun_out/bench_$tag.json 2>/dev/null; echo "bench $tag rc=$?"
 done
