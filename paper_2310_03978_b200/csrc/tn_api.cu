@@ -1199,16 +1199,29 @@ tn_status build_plan(tn_ctx* c) {
   // producer of one operand so that its epilogue can write the operand's fp16 planes
   // in 16-B vectors; default: sorted by label
   std::vector<std::vector<int64_t>> korder(n_steps);
+  // per step: log2-ish size of its output and the producer / size of its consumer's other
+  // operand, so that the producer of a consumer's BIGGER operand fixes the K order (its
+  // planes are the ones worth writing from the epilogue; the small side is transposed)
+  std::vector<double> out_size(n_steps, 0.0), other_size(n_steps, 0.0);
+  std::vector<int> other_prod(n_steps, -1);
   {
     std::vector<std::unordered_set<int64_t>> lab(n_leaves);
     std::vector<int> producer(n_leaves, -1);
     for (int t = 0; t < n_leaves; ++t)
       for (auto& d : live[t].dims)
         if (d.label != GROUP) lab[t].insert(d.label);
+    auto size_of = [&](const std::unordered_set<int64_t>& L) {
+      double z = 1.0;
+      for (int64_t x : L) { auto it = c->dim_of.find(x); if (it != c->dim_of.end()) z *= (double)it->second; }
+      return z;
+    };
     for (int s = 0; s < n_steps; ++s) {
       const int i = c->path[s].first, j = c->path[s].second;
       std::unordered_set<int64_t> shared;
       for (int64_t x : lab[i]) if (lab[j].count(x)) shared.insert(x);
+      const double zi = size_of(lab[i]), zj = size_of(lab[j]);
+      if (producer[i] >= 0) { other_prod[producer[i]] = producer[j]; other_size[producer[i]] = zj; }
+      if (producer[j] >= 0) { other_prod[producer[j]] = producer[i]; other_size[producer[j]] = zi; }
       if (producer[i] >= 0) { consumer_k[producer[i]] = shared; consumer_step[producer[i]] = s; }
       if (producer[j] >= 0) { consumer_k[producer[j]] = shared; consumer_step[producer[j]] = s; }
       std::unordered_set<int64_t> out;
@@ -1217,8 +1230,10 @@ tn_status build_plan(tn_ctx* c) {
       lab[i] = out;
       lab[j].clear();
       producer[i] = s;
+      out_size[s] = size_of(out);
     }
   }
+  const int korder_big = env_int("TN_KORDER_BIG", 1);   // 0: the first producer decides (round 1-2)
   // Which producers write their output in the consumer's order (index reordering).
   c->reorder_mode = env_int("TN_REORDER", 2);
   c->reorder_topk = env_int("TN_REORDER_TOPK", 10);
@@ -1507,7 +1522,9 @@ tn_status build_plan(tn_ctx* c) {
         const bool q_inner = eq >= 8 || ep < 8;
         for (auto& d : (q_inner ? conp : conq)) con.push_back(d);
         for (auto& d : (q_inner ? conq : conp)) con.push_back(d);
-        if (consumer_step[s] >= 0) {
+        // a later producer of the consumer's >= 4x bigger operand decides instead
+        const bool defer = korder_big && other_prod[s] > s && other_size[s] >= 4.0 * out_size[s];
+        if (consumer_step[s] >= 0 && !defer) {
           std::vector<int64_t>& ko = korder[consumer_step[s]];
           if (ko.empty()) {            // the consumer's first tensor-core producer decides
             for (auto& d : con) ko.push_back(d.label);
