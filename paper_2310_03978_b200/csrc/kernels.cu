@@ -990,6 +990,8 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
   // every warp access stays lane-coalesced): R·KU·VEC·8 B in flight per thread
   constexpr int KU = R == 4 ? 4 : (R == 2 ? (VEC == 2 ? 4 : 8) : (NMAX <= 16 ? 8 : 4));
   const int64_t V = d.V, Vv = V / VEC, Mb = d.M / VEC, Mv = d.J * Mb;
+  const bool vv_p2 = (Vv & (Vv - 1)) == 0, mb_p2 = (Mb & (Mb - 1)) == 0;
+  const int lvv = __ffsll(Vv) - 1, lmb = __ffsll(Mb) - 1;
   const int64_t vstride = d.m_sa[d.nm - 1];
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   float amax = 0.f;
@@ -1004,10 +1006,11 @@ __global__ void __launch_bounds__(256) einsum_skinny_kernel(const EinsumDesc* __
       live[r] = m < Mv;
       int64_t mm = live[r] ? m : m0, jb = 0;
       if (d.J > 1) {
-        jb = mm / Mb;
+        jb = mb_p2 ? (mm >> lmb) : mm / Mb;
         mm -= jb * Mb;
       }
-      const int64_t vi = (mm % Vv) * VEC, o = mm / Vv;
+      // power-of-two extents: shifts instead of 64-bit division (emulated, ~100 instructions)
+      const int64_t vi = (vv_p2 ? (mm & (Vv - 1)) : (mm % Vv)) * VEC, o = vv_p2 ? (mm >> lvv) : mm / Vv;
       a_row[r] = A + (d.J > 1 ? (int64_t)d.ia[jb] * d.a_gs : 0) +
                  (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa) : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) +
                  vi * vstride;
@@ -1123,11 +1126,13 @@ __global__ void __launch_bounds__(256) einsum_wide_kernel(const EinsumDesc* __re
   }
   __syncthreads();
   const int64_t V = d.V, Vv = V / VEC, Mv = d.M / VEC;
+  const bool vv_p2 = (Vv & (Vv - 1)) == 0;
+  const int lvv = __ffsll(Vv) - 1;
   const int64_t vstride = d.m_sa[d.nm - 1];
   float amax = 0.f;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mv;
        m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = (m % Vv) * VEC, o = m / Vv;
+    const int64_t vi = (vv_p2 ? (m & (Vv - 1)) : (m % Vv)) * VEC, o = vv_p2 ? (m >> lvv) : m / Vv;
     const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
     float2 a[KMAX][VEC];
     if (KP == 2) {         // (k, k+1) adjacent in A: 16-B loads
@@ -1214,6 +1219,8 @@ __global__ void __launch_bounds__(256) einsum_skinny_old_kernel(const EinsumDesc
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
   __syncthreads();
   const int64_t V = d.V;
+  const bool vp2 = (V & (V - 1)) == 0;
+  const int lv = __ffsll(V) - 1;
   const int64_t vstride = d.m_sa[d.nm - 1];
   // U rows per thread per iteration (independent loads in flight); U = 2 while
   // the accumulators fit comfortably in registers
@@ -1229,7 +1236,7 @@ __global__ void __launch_bounds__(256) einsum_skinny_old_kernel(const EinsumDesc
       const int64_t m = m0 + u * step;
       live[u] = m < d.M;
       const int64_t mm = live[u] ? m : m0;
-      const int64_t vi = mm % V, o = mm / V;
+      const int64_t vi = POW2 ? (mm & (V - 1)) : mm % V, o = POW2 ? (mm >> lv) : mm / V;
       a_row[u] = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
                            : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi * vstride;
       obase[u] = o * N * V + vi;
@@ -1288,10 +1295,11 @@ __global__ void __launch_bounds__(256) einsum_skinny2_old_kernel(const EinsumDes
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff[k] = decompose(k, d.nk, d.k_ext, d.k_sa);
   __syncthreads();
   const int64_t V = d.V, Vh = V / 2, Mh = d.M / 2;
+  const int lvh = __ffsll(Vh) - 1;
   float amax = 0.f;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < Mh;
        m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = (m % Vh) * 2, o = m / Vh;
+    const int64_t vi = (POW2 ? (m & (Vh - 1)) : (m % Vh)) * 2, o = POW2 ? (m >> lvh) : m / Vh;
     const float2* a_row = A + (POW2 ? decompose_sh(o, d.nm - 1, d.m_sh, d.m_sa)
                                     : decompose(o, d.nm - 1, d.m_ext, d.m_sa)) + vi;
     float r0[NMAX], i0[NMAX], r1[NMAX], i1[NMAX];
@@ -1348,11 +1356,13 @@ __global__ void __launch_bounds__(256) einsum_wide_old_kernel(const EinsumDesc* 
   }
   __syncthreads();
   const int64_t V = d.V;
+  const bool vp2 = (V & (V - 1)) == 0;
+  const int lv = __ffsll(V) - 1;
   const int64_t vstride = d.m_sa[d.nm - 1];
   float amax = 0.f;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < d.M;
        m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vi = m % V, o = m / V;
+    const int64_t vi = vp2 ? (m & (V - 1)) : m % V, o = vp2 ? (m >> lv) : m / V;
     const float2* a_row = A + decompose(o, d.nm - 1, d.m_ext, d.m_sa) + vi * vstride;
     float2 a[KMAX];
 #pragma unroll
