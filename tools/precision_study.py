@@ -7,7 +7,13 @@ Fig. 4 set on B200:
   - 1xTF32 / 3xTF32 (Eq. 8 as printed; tcgen05 kind::tf32, RN split),
   - 1xBF16 / 3xBF16 (kind::f16 with bf16 operands, RN split),
   - 1xFP16 / 3xFP16 with power-of-two rescaling (this library's mixed / extended mode),
-  - the library's SIMT path (fp32 products, fp64 sums).
+  - the library's SIMT path (fp32 products, fp64 sums),
+  - an Ozaki-scheme emulation on the same tensor cores: every row of A and B is split
+    into 8 slices of 4-bit integers under a per-row power of two; the slice products
+    with i + j <= 7 (36 one-pass fp16 GEMMs through tn_cgemm) are exact, because their
+    integer sums stay below 2^24 and the fp32 TMEM accumulator then never rounds; they
+    are combined in fp64 on the host (an error-free transformation up to the dropped
+    slices).
 
     python tools/precision_study.py [--k 16384] [--out file.json]"""
 import argparse
@@ -40,6 +46,45 @@ def operands(rng, m, n, k, magnitude):
     return one(m).astype(np.complex64), one(n).astype(np.complex64)
 
 
+OZ_BITS, OZ_SLICES = 4, 8
+
+
+def ozaki_split(X):
+    """Row-wise split X[r] = 2^e_r * sum_s S_s[r] * 2^(-4 (s+1)), S_s complex with integer
+    parts |.| < 16 (exact in fp16), 8 slices; the remainder is below 2^-32 of the row max."""
+    X = X.astype(np.complex128)
+    amax = np.maximum(np.abs(X.real), np.abs(X.imag)).max(axis=1)
+    e = np.floor(np.log2(np.where(amax > 0, amax, 1.0))) + 1.0      # |X / 2^e| < 1
+    Y = X / 2.0 ** e[:, None]
+    slices = []
+    for _ in range(OZ_SLICES):
+        Y = Y * 2.0 ** OZ_BITS
+        S = np.trunc(Y.real) + 1j * np.trunc(Y.imag)
+        slices.append(S.astype(np.complex64))
+        Y = Y - S
+    return e, slices
+
+
+def ozaki_gemm(ctx, A32, B32):
+    """C = A B^T from exact one-pass fp16 tensor-core products of 4-bit slices (k <= 2^14:
+    each complex slice product sums < 2 * 2^8 * 2^14 = 2^23 < 2^24, so the fp32
+    accumulator holds the integers exactly)."""
+    m, k = A32.shape
+    n = B32.shape[0]
+    assert k <= 1 << 14
+    ea, sa = ozaki_split(A32)
+    eb, sb = ozaki_split(B32)
+    C = np.zeros((m, n), np.complex128)
+    for i in range(OZ_SLICES):
+        tA = torch.from_numpy(sa[i]).cuda().reshape(1, m, k)
+        for j in range(OZ_SLICES - i):     # i + j <= OZ_SLICES - 1
+            tB = torch.from_numpy(sb[j]).cuda().reshape(1, n, k)
+            tC = torch.empty(1, m, n, dtype=torch.complex64, device="cuda")
+            ctx.cgemm(tA, tB, tC, 1, m, n, k, passes=1, fmt="fp16")
+            C += tC[0].cpu().numpy().astype(np.complex128) * 2.0 ** (-OZ_BITS * (i + j + 2))
+    return C * 2.0 ** ea[:, None] * 2.0 ** eb[None, :]
+
+
 def study(ctx, k=16384, m=128, n=128, magnitudes=tuple(10.0 ** e for e in range(-7, 4)) + (None,),
           seed=5):
     rng = np.random.default_rng(seed)
@@ -62,6 +107,7 @@ def study(ctx, k=16384, m=128, n=128, magnitudes=tuple(10.0 ** e for e in range(
         res["fp32_cuda_core"] = rel((tA[0] @ tB[0].T).cpu().numpy().astype(np.complex128), ref)
         torch.backends.cuda.matmul.allow_tf32 = prev
         res["fp32_numpy"] = rel((A32 @ B32.T).astype(np.complex128), ref)
+        res["ozaki_fp16"] = rel(ozaki_gemm(ctx, A32, B32), ref)
         rows.append(res)
     return rows
 
